@@ -1,0 +1,142 @@
+"""Seeded synthetic workloads shaped like the paper's.
+
+* Items: N distinct ND-tuples drawn uniformly from [0, V)^ND without replacement. Item i is the
+  base-V digit expansion of pi(i), where pi is a keyed Feistel permutation of [0, V^ND) (4 rounds,
+  splitmix64 round function, cycle-walking when the domain has an odd number of bits). The paper
+  gives no item distribution (section 9.1 uses real datasets), so uniform is a declared
+  choice. The list is returned UNSORTED in generation order; `dup_frac` appends duplicates and
+  shuffles, to exercise de-duplication.
+* Logits: i.i.d. fp32 x = sigma * z, z ~ N(0, 1) from numpy's PCG64 (sigma = 2 "flat", 4 "peaky").
+  Multiplying by a power of two is exact, so the bytes are fully determined by (seed, shape, sigma).
+* Prefix-keyed logits (tiny exhaustive tests): x(prefix, v) is an Irwin-Hall(4) sum of 16-bit
+  fields of splitmix64(seed, request, prefix, v), times 2^-15: exactly representable in fp32 and
+  bit-identical in any language.
+
+Nothing here computes any part of the beam-search method.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+# BASELINE.json "configs", in order. n_items for C4 is SURVEY.md's proposal (BASELINE gives none).
+CONFIGS = {
+    "C1": dict(batch=1, beam_width=4, vocab=16, nd=3, n_items=200),
+    "C2": dict(batch=64, beam_width=128, vocab=8192, nd=3, n_items=10_000_000),
+    "C3": dict(batch=256, beam_width=256, vocab=8192, nd=3, n_items=100_000_000),
+    "C4": dict(batch=512, beam_width=512, vocab=16384, nd=4, n_items=100_000_000),
+    "C5": dict(batch=128, beam_width=512, vocab=65536, nd=3, n_items=1_000_000_000),
+}
+
+
+def config(name: str) -> dict:
+    c = dict(CONFIGS[name])
+    c["name"] = name
+    c["trie_key"] = config_key(name)
+    return c
+
+
+def splitmix64(x):
+    """splitmix64 finaliser on uint64 (numpy array or python int). Wrapping arithmetic."""
+    scalar = not isinstance(x, np.ndarray)
+    z = np.asarray(x, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = z + np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    return int(z) if scalar else z
+
+
+def config_key(name: str) -> int:
+    k = int(name[1:])
+    return splitmix64(2512115290 + k)
+
+
+def _feistel_round_keys(key: int, rounds: int):
+    return [np.uint64(splitmix64((key + 0x632BE59BD9B4E019 * (r + 1)) & 0xFFFFFFFFFFFFFFFF))
+            for r in range(rounds)]
+
+
+def feistel_permute(i: np.ndarray, bits: int, key: int, rounds: int = 4) -> np.ndarray:
+    """Keyed pseudorandom permutation of [0, 2^bits) applied to uint64 array i (values < 2^bits).
+
+    Feistel network with halves of a = floor(bits/2) and b = bits - a bits (unbalanced when bits
+    is odd: the halves swap widths every round). Each round (L, R) -> (R, L ^ F(R)) is invertible,
+    so the composition is a bijection of [0, 2^bits) with no cycle walking.
+    """
+    assert 2 <= bits <= 64 and rounds % 2 == 0
+    a = bits // 2
+    b = bits - a
+    rk = _feistel_round_keys(key, rounds)
+    v = np.asarray(i, dtype=np.uint64)
+    la, lb = a, b                      # widths of (L, R)
+    left = v >> np.uint64(lb)
+    right = v & np.uint64((1 << lb) - 1)
+    for r in range(rounds):
+        f = splitmix64(right ^ rk[r])
+        f &= np.uint64((1 << la) - 1)
+        left ^= f
+        left, right = right, left      # new L has lb bits, new R has la bits
+        la, lb = lb, la
+    return (left << np.uint64(lb)) | right
+
+
+def make_items(n: int, vocab: int, nd: int, key: int, dup_frac: float = 0.0,
+               shuffle_seed: int | None = None, chunk: int = 1 << 24) -> np.ndarray:
+    """N distinct uniform ND-tuples over [0, vocab) as int32 [n (+dups)][nd], unsorted."""
+    assert vocab >= 2 and (vocab & (vocab - 1)) == 0, "generator needs a power-of-two vocab"
+    b = vocab.bit_length() - 1
+    bits = b * nd
+    assert n <= (1 << bits), "more items than distinct tuples"
+    out = np.empty((n, nd), dtype=np.int32)
+    vm = np.uint64(vocab - 1)
+    for s in range(0, n, chunk):
+        e = min(n, s + chunk)
+        y = feistel_permute(np.arange(s, e, dtype=np.uint64), bits, key)
+        for d in range(nd):
+            out[s:e, d] = ((y >> np.uint64(b * (nd - 1 - d))) & vm).astype(np.int32)
+    if dup_frac > 0.0:
+        rng = np.random.default_rng(shuffle_seed if shuffle_seed is not None else key & 0xFFFFFFFF)
+        nd_ = max(1, int(n * dup_frac))
+        dups = out[rng.integers(0, n, size=nd_)]
+        out = np.concatenate([out, dups], axis=0)
+        out = out[rng.permutation(out.shape[0])]
+        out = np.ascontiguousarray(out)
+    return out
+
+
+def make_logits(shape, seed: int, sigma: float = 2.0) -> np.ndarray:
+    """fp32 i.i.d. N(0, sigma^2) logits of the given shape (numpy PCG64, seeded)."""
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal(size=shape, dtype=np.float32)
+    x *= np.float32(sigma)
+    return x
+
+
+def make_logits_torch(shape, seed: int, sigma: float = 2.0, device="cuda"):
+    """Device-side generator for large bench inputs (torch Philox, seeded). Not bit-equal to
+    make_logits; parity at full size D2H-copies what this produced."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) & 0x7FFFFFFFFFFFFFFF)
+    x = torch.randn(shape, generator=g, device=device, dtype=torch.float32)
+    x.mul_(float(sigma))
+    return x
+
+
+def prefix_keyed_row(seed: int, request: int, prefix, vocab: int) -> np.ndarray:
+    """fp32 row x(prefix, v) for v < vocab: Irwin-Hall(4) of 16-bit fields of a splitmix64 hash,
+    scaled by 2^-15 (exact). Same prefix -> same row, whatever slot it sits in."""
+    h = splitmix64((seed * 0x9E3779B1 + request) & 0xFFFFFFFFFFFFFFFF)
+    for t in prefix:
+        h = splitmix64((h ^ (int(t) + 0x51ED27)) & 0xFFFFFFFFFFFFFFFF)
+    h = splitmix64((h + len(prefix)) & 0xFFFFFFFFFFFFFFFF)
+    v = np.arange(vocab, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        r = splitmix64(v ^ np.uint64(h))
+    s = np.zeros(vocab, dtype=np.int64)
+    for k in range(4):
+        s += ((r >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.int64)
+    return ((s - 131070).astype(np.float32) * np.float32(2.0 ** -15)).astype(np.float32)

@@ -1,0 +1,180 @@
+/*
+ * xgr_beam.h -- C ABI of the B200-native xBeam decode-step selection library.
+ *
+ * The operation (PAPER.md = /root/reference/PAPER.md, line numbers L<n>):
+ *   Per request and decode step t = 1..ND, the live beams' next-token logits are filtered to the
+ *   legal children of each beam's prefix in the pre-built item trie ("valid path constraint",
+ *   L361, section 6.1; dense/sparse mask storage, L371), normalised by an fp32 log-softmax over
+ *   the legal tokens, added to the running beam score ("accumulates log-probabilities", L376,
+ *   section 6.2) and the global Top-BW (parent beam, token) pairs are kept (L154-156, section
+ *   2.2.2; L356, section 6), with early termination against a running BW-th threshold (L376-385,
+ *   section 6.2) and fixed, reused beam structures (L392, section 6.3). After ND steps the TID
+ *   tuples are the item IDs (L309, section 5).
+ *   Exact result (readings R1-R21): the first min(BW, #legal) candidates under
+ *   (S_b + x_{b,v} - LSE_{u in L_b} x_{b,u}) descending, ties to the lower flat index b*V + v.
+ *
+ * Sequencing: xgr_beam_init -> xgr_mask_build (once; the trie is immutable and reused) ->
+ *   { exactly nd x xgr_beam_step -> xgr_beam_finalize } repeated per batch -> xgr_beam_destroy.
+ *   Violations return XGR_ERR_SEQUENCE.
+ *
+ * Memory / ownership: the ctx owns the device trie and a fixed workspace sized at init for
+ *   max_batch requests ("does not allocate entirely new data structure"):
+ *   xgr_beam_step and xgr_beam_finalize never allocate. Pointers passed in are borrowed; device
+ *   inputs must stay valid until the stream work completes.
+ *
+ * Streams: `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   xgr_beam_step validates on the host and only enqueues work: no host synchronisation, no
+ *   allocation, so it can be captured in a CUDA graph.
+ *
+ * Errors: every call returns xgr_status; xgr_last_error() gives a thread-local message. Nothing
+ *   aborts or exits. Device-detected NaN/+Inf logits at legal positions (or a row whose legal
+ *   logits are all -Inf) set a sticky per-request flag reported by xgr_beam_request_status and
+ *   by xgr_beam_finalize(..., outputs_on_device = 0) as XGR_ERR_NONFINITE; that request's output
+ *   is undefined, other requests are unaffected. A legal -Inf logit is a zero-probability token.
+ *
+ * Threading: a ctx is single-stream and not thread-safe; distinct ctxs are independent.
+ */
+#ifndef XGR_BEAM_H
+#define XGR_BEAM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define XGR_ABI_VERSION 1
+
+typedef struct xgr_ctx xgr_ctx; /* opaque; one per in-flight batch */
+
+typedef enum {
+  XGR_OK = 0,
+  XGR_ERR_INVALID_ARG = 1, /* null pointer, size out of range, bad config */
+  XGR_ERR_UNSUPPORTED = 2, /* valid but not implemented (0 < top_k < BW, nranks > 1, ...) */
+  XGR_ERR_TOKEN_RANGE = 3, /* mask_build: a token < 0 or >= V */
+  XGR_ERR_EMPTY_VOCAB = 4, /* mask_build: zero items (no beam could live) */
+  XGR_ERR_SEQUENCE = 5,    /* call out of order */
+  XGR_ERR_ALIGNMENT = 6,   /* logits not 16-byte aligned or ld % 4 != 0 */
+  XGR_ERR_NONFINITE = 7,   /* a request saw NaN/+Inf at a legal position */
+  XGR_ERR_CUDA = 8,
+  XGR_ERR_NCCL = 9,
+  XGR_ERR_OOM = 10
+} xgr_status;
+
+/* config.flags */
+#define XGR_CFG_NO_PRUNE 0x1u /* theta = -inf: every legal candidate survives (test/ablation) */
+#define XGR_CFG_COUNTERS 0x2u /* accumulate device counters (xgr_beam_counters) */
+#define XGR_CFG_NO_SPARSE_KERNEL 0x4u /* route every step through the dense-step kernels */
+
+typedef struct {
+  int32_t vocab;      /* V: tokens per level, 1..65536                                   */
+  int32_t nd;         /* ND: tokens per item (trie depth), 1..8; nd*ceil(log2 V) <= 64    */
+  int32_t beam_width; /* BW, 1..1024                                                      */
+  int32_t top_k;      /* per-beam K. 0 or >= BW: no truncation (v1 only)  */
+  int32_t max_batch;  /* max requests per step call, >= 1                                 */
+  int32_t device;     /* CUDA device ordinal                                             */
+  int32_t nranks;     /* codebook shards; v1: must be 1                                   */
+  int32_t rank;       /* v1: must be 0                                                    */
+  const void* nccl_id;/* reserved for the codebook shard (ncclUniqueId); NULL in v1      */
+  int32_t survivor_cap; /* per-request survivor buffer (keys); 0 = min(32*BW, 16384)      */
+  int32_t theta_rows;   /* rows 0..theta_rows-1 seed the threshold; 0 = default (8)       */
+  uint32_t flags;       /* XGR_CFG_*                                                      */
+  int32_t reserved[5];  /* must be zero                                                   */
+} xgr_config;
+
+/* Create a context: validates cfg, selects the device, allocates the fixed beam workspace
+ * (O(max_batch * BW * (nd + survivor_cap)) bytes). *out is NULL on failure. */
+xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out);
+
+/* Build the device trie of legal items ("pre-built valid item vocabulary", PAPER.md L361;
+ * "pre-generated during model loading", L371). items: HOST int32 [n_items][nd], any order;
+ * duplicates are removed silently. Per level: nodes = distinct prefixes numbered in
+ * lexicographic order, first_child offsets, each node's token label, and for nodes with
+ * >= V/16 children a dense V-bit bitmap with a rank directory (otherwise the sorted labels of
+ * its children act as the sparse list). Leaf id at level nd = the item's rank in the sorted,
+ * de-duplicated list. Synchronous: returns after the build completed on `stream`.
+ * Errors: XGR_ERR_TOKEN_RANGE, XGR_ERR_EMPTY_VOCAB, XGR_ERR_INVALID_ARG (n_items >= 2^32),
+ * XGR_ERR_SEQUENCE (already built), XGR_ERR_OOM. */
+xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, void* stream);
+
+/* One decode step for `batch` requests (step t = number of previous steps + 1).
+ * logits: DEVICE fp32 [batch][rows][ld], request r's row b at logits + (r*rows + b)*ld; row b is
+ *   the next-token distribution of live slot b of the previous step (slot 0 = the root at t=1).
+ *   Rows >= n_live and columns outside the legal set are never read. 16-byte aligned, ld % 4 == 0,
+ *   ld >= V. At t = 1 rows >= 1 (only row 0 is read); at t > 1 rows >= BW.
+ * batch: 1..max_batch, fixed by the first step of a batch.
+ * Enqueues only (no sync, no allocation); graph-capturable. */
+xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows,
+                         int64_t ld, void* stream);
+
+/* After exactly nd steps: item tuples of the final beams, in slot order (score descending).
+ * tokens [batch][BW][nd] int32, item_rank [batch][BW] int64 (rank in the sorted de-duplicated
+ * item list), score [batch][BW] fp32 (sum of the per-step log-probabilities), n_live [batch].
+ * Dead slots (n_live <= j < BW): tokens/item_rank -1, score -inf. Any output pointer may be NULL.
+ * outputs_on_device != 0: pointers are device memory, call only enqueues.
+ * outputs_on_device == 0: host memory; synchronises `stream`; returns XGR_ERR_NONFINITE if a
+ * request was flagged. Resets the ctx for the next batch (the trie is kept). */
+xgr_status xgr_beam_finalize(xgr_ctx* ctx, int32_t* tokens, int64_t* item_rank, float* score,
+                             int32_t* n_live, int32_t outputs_on_device, void* stream);
+
+xgr_status xgr_beam_destroy(xgr_ctx* ctx);
+const char* xgr_last_error(void);
+int32_t xgr_abi_version(void);
+
+/* ---- support calls (tests, parity, accounting) ---------------------------------------- */
+
+/* Device pointers to the latest step's beam state, each [batch][BW] (node ids are the trie
+ * node of each slot's prefix at level t). Valid until the next step/finalize. */
+xgr_status xgr_beam_view(const xgr_ctx* ctx, const int32_t** parent, const int32_t** token,
+                         const float** score, const int32_t** n_live, const uint32_t** node);
+
+/* Device pointers to step t's (1-based) parent/token history, each [batch][BW]. */
+xgr_status xgr_beam_history(const xgr_ctx* ctx, int32_t step, const int32_t** parent,
+                            const int32_t** token);
+
+/* Per-request sticky status bits of the current batch, copied to HOST flags[batch]
+ * (bit 0: non-finite logit, bit 1: survivor overflow -> exact fallback taken). Synchronous. */
+xgr_status xgr_beam_request_status(const xgr_ctx* ctx, uint32_t* flags, int32_t batch,
+                                   void* stream);
+
+/* Legal children of n HOST prefixes [n][depth] (depth < nd), read from the representation the
+ * step kernels use (dense bitmap or sparse labels). counts[i] = number of children (-1 if the
+ * prefix is not in the trie, -2 if the node's rank/label views disagree); tokens[i][0..cap) the
+ * first min(count, cap) children ascending. HOST outputs; synchronous. */
+xgr_status xgr_mask_children(const xgr_ctx* ctx, const int32_t* prefixes, int32_t depth,
+                             int64_t n, int32_t* counts, int32_t* tokens, int64_t cap,
+                             void* stream);
+
+/* Trie shape: n_items (after de-dup), nodes_per_level[nd+1], dense_per_level[nd+1] (levels
+ * 0..nd; leaves are never dense), max_children_per_level[nd+1], device bytes held by the trie.
+ * Any pointer may be NULL. */
+xgr_status xgr_mask_info(const xgr_ctx* ctx, int64_t* n_items, int64_t* nodes_per_level,
+                         int64_t* dense_per_level, int64_t* max_children_per_level,
+                         int64_t* trie_bytes);
+
+/* Device counters accumulated since the last call (needs XGR_CFG_COUNTERS), copied to HOST
+ * out[XGR_NUM_COUNTERS], then zeroed. Synchronous. */
+#define XGR_NUM_COUNTERS 8
+#define XGR_CNT_ROWS_READ 0      /* rows whose logits were streamed by the dense-step pass   */
+#define XGR_CNT_ROWS_SKIP_PRE 1  /* rows skipped before reading (S_b < theta)               */
+#define XGR_CNT_ROWS_SKIP_POST 2 /* rows read but emitting nothing (S_b - ln Z_b < theta)   */
+#define XGR_CNT_LEGAL 3          /* legal candidates of the rows read                       */
+#define XGR_CNT_SURVIVORS 4      /* candidates emitted to the per-request survivor buffers  */
+#define XGR_CNT_OVERFLOW 5       /* requests that took the exact overflow fallback          */
+#define XGR_CNT_SPARSE_CANDS 6   /* candidates handled by the sparse-step kernel            */
+#define XGR_CNT_DENSE_STEPS 7    /* (request, step) pairs run through the dense-step path   */
+xgr_status xgr_beam_counters(xgr_ctx* ctx, uint64_t* out, void* stream);
+
+/* Algorithmic HBM bytes of the LAST step: over live rows b with
+ * S_b >= theta* (theta* = the BW-th selected score of that request): 32 B per 32-byte logit
+ * sector holding >= 1 legal token, plus the mask bytes of the distinct dense nodes touched
+ * (V/8 each) or 4 + 2|L| per sparse row, plus 16 B of state per row. Also the "full" bytes
+ * (every live row, whole V). Host outputs; synchronous; not for the timed path. */
+xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_bytes,
+                            int64_t* legal_candidates, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XGR_BEAM_H */

@@ -1,0 +1,294 @@
+"""Thin ctypes binding over libxgr_beam.so (include/xgr_beam.h). Argument marshalling only:
+every step of the path runs in the library's CUDA kernels. torch is used for device memory and
+streams. There is no CPU fallback: if the library is missing this module fails to import.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libxgr_beam.so")
+
+XGR_OK = 0
+STATUS_NAMES = {
+    0: "XGR_OK", 1: "XGR_ERR_INVALID_ARG", 2: "XGR_ERR_UNSUPPORTED", 3: "XGR_ERR_TOKEN_RANGE",
+    4: "XGR_ERR_EMPTY_VOCAB", 5: "XGR_ERR_SEQUENCE", 6: "XGR_ERR_ALIGNMENT",
+    7: "XGR_ERR_NONFINITE", 8: "XGR_ERR_CUDA", 9: "XGR_ERR_NCCL", 10: "XGR_ERR_OOM",
+}
+XGR_CFG_NO_PRUNE = 0x1
+XGR_CFG_COUNTERS = 0x2
+XGR_CFG_NO_SPARSE_KERNEL = 0x4
+XGR_NUM_COUNTERS = 8
+COUNTER_NAMES = ["rows_read", "rows_skip_pre", "rows_skip_post", "legal", "survivors",
+                 "overflow", "sparse_cands", "dense_steps"]
+
+# every symbol include/xgr_beam.h declares
+EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_finalize",
+           "xgr_beam_destroy", "xgr_last_error", "xgr_abi_version", "xgr_beam_view",
+           "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
+           "xgr_beam_counters", "xgr_beam_account"]
+
+
+class XgrConfig(ctypes.Structure):
+    _fields_ = [
+        ("vocab", ctypes.c_int32), ("nd", ctypes.c_int32), ("beam_width", ctypes.c_int32),
+        ("top_k", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("device", ctypes.c_int32),
+        ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+        ("survivor_cap", ctypes.c_int32), ("theta_rows", ctypes.c_int32),
+        ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 5),
+    ]
+
+
+class XgrError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS_NAMES.get(status, str(status))
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; "
+                          "g.build()'` (the CUDA library is required; there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I32, I64, VP = ctypes.POINTER, ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p
+    sig = {
+        "xgr_beam_init": [P(XgrConfig), P(VP)],
+        "xgr_mask_build": [VP, VP, I64, VP],
+        "xgr_beam_step": [VP, I32, VP, I32, I64, VP],
+        "xgr_beam_finalize": [VP, VP, VP, VP, VP, I32, VP],
+        "xgr_beam_destroy": [VP],
+        "xgr_beam_view": [VP, P(VP), P(VP), P(VP), P(VP), P(VP)],
+        "xgr_beam_history": [VP, I32, P(VP), P(VP)],
+        "xgr_beam_request_status": [VP, VP, I32, VP],
+        "xgr_mask_children": [VP, VP, I32, I64, VP, VP, I64, VP],
+        "xgr_mask_info": [VP, VP, VP, VP, VP, VP],
+        "xgr_beam_counters": [VP, VP, VP],
+        "xgr_beam_account": [VP, VP, VP, VP, VP],
+    }
+    for name, args in sig.items():
+        f = getattr(lib, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    lib.xgr_last_error.argtypes = []
+    lib.xgr_last_error.restype = ctypes.c_char_p
+    lib.xgr_abi_version.argtypes = []
+    lib.xgr_abi_version.restype = ctypes.c_int32
+    return lib
+
+
+lib = _load()
+
+
+def _check(st: int):
+    if st != XGR_OK:
+        raise XgrError(st, lib.xgr_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return lib.xgr_last_error().decode(errors="replace")
+
+
+# ---- thin wrappers with the C names -------------------------------------------------------------
+def xgr_beam_init(cfg: XgrConfig) -> ctypes.c_void_p:
+    h = ctypes.c_void_p()
+    _check(lib.xgr_beam_init(ctypes.byref(cfg), ctypes.byref(h)))
+    return h
+
+
+def xgr_mask_build(ctx, items: np.ndarray, stream=0):
+    items = np.ascontiguousarray(items, dtype=np.int32)
+    n = items.shape[0] if items.ndim >= 1 else 0
+    _check(lib.xgr_mask_build(ctx, items.ctypes.data if n else None, n, stream))
+
+
+def xgr_beam_step(ctx, batch, logits_ptr, rows, ld, stream=0):
+    _check(lib.xgr_beam_step(ctx, batch, logits_ptr, rows, ld, stream))
+
+
+def xgr_beam_finalize(ctx, tokens, item_rank, score, n_live, outputs_on_device, stream=0):
+    return lib.xgr_beam_finalize(ctx, tokens, item_rank, score, n_live, outputs_on_device, stream)
+
+
+def xgr_beam_destroy(ctx):
+    _check(lib.xgr_beam_destroy(ctx))
+
+
+def xgr_mask_children(ctx, prefixes: np.ndarray, depth: int, cap: int, stream=0):
+    prefixes = np.ascontiguousarray(prefixes, dtype=np.int32).reshape(-1, max(depth, 1))
+    n = prefixes.shape[0] if depth > 0 else prefixes.shape[0]
+    counts = np.zeros(n, dtype=np.int32)
+    toks = np.zeros((n, max(cap, 1)), dtype=np.int32)
+    _check(lib.xgr_mask_children(ctx, prefixes.ctypes.data if depth > 0 else None, depth, n,
+                                 counts.ctypes.data, toks.ctypes.data, cap, stream))
+    return counts, toks[:, :cap]
+
+
+def xgr_mask_info(ctx, nd: int):
+    n = ctypes.c_int64()
+    nodes = np.zeros(nd + 1, np.int64)
+    dense = np.zeros(nd + 1, np.int64)
+    maxc = np.zeros(nd + 1, np.int64)
+    b = ctypes.c_int64()
+    _check(lib.xgr_mask_info(ctx, ctypes.byref(n), nodes.ctypes.data, dense.ctypes.data,
+                             maxc.ctypes.data, ctypes.byref(b)))
+    return {"n_items": n.value, "nodes": nodes, "dense": dense, "max_children": maxc,
+            "bytes": b.value}
+
+
+# ---- zero-copy torch views of library-owned device buffers --------------------------------------
+class _CudaArray:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _view(ptr, shape, typestr, device):
+    import torch
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
+
+
+class BeamSearch:
+    """xBeam decode-step selection for one in-flight batch (wraps one xgr_ctx).
+
+    Usage: bs = BeamSearch(V, ND, BW, max_batch); bs.mask_build(items);
+           for t in range(ND): bs.step(logits_t); out = bs.finalize()
+    """
+
+    def __init__(self, vocab: int, nd: int, beam_width: int, max_batch: int, device: int = 0,
+                 flags: int = 0, survivor_cap: int = 0, theta_rows: int = 0, top_k: int = 0):
+        import torch
+        self.vocab, self.nd, self.bw, self.max_batch = vocab, nd, beam_width, max_batch
+        self.device = torch.device("cuda", device)
+        cfg = XgrConfig()
+        cfg.vocab, cfg.nd, cfg.beam_width, cfg.top_k = vocab, nd, beam_width, top_k
+        cfg.max_batch, cfg.device, cfg.nranks, cfg.rank = max_batch, device, 1, 0
+        cfg.survivor_cap, cfg.theta_rows, cfg.flags = survivor_cap, theta_rows, flags
+        self.ctx = xgr_beam_init(cfg)
+        self.batch = None
+        self.t = 0
+        self._staging = None
+
+    def close(self):
+        if self.ctx:
+            xgr_beam_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _stream(stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return ctypes.c_void_p(s.cuda_stream)
+
+    def mask_build(self, items: np.ndarray, stream=None):
+        xgr_mask_build(self.ctx, items, self._stream(stream))
+
+    def info(self):
+        return xgr_mask_info(self.ctx, self.nd)
+
+    def children(self, prefixes, depth: int, cap: int):
+        return xgr_mask_children(self.ctx, np.asarray(prefixes), depth, cap, self._stream())
+
+    def step(self, logits, stream=None):
+        """logits: fp32 [batch][rows][ld] (or [batch][rows][V]); CUDA tensor, or a pinned CPU
+        tensor, which is copied into a device staging buffer on the same stream first."""
+        import torch
+        if logits.dim() != 3 or logits.dtype != torch.float32:
+            raise ValueError("logits must be fp32 [batch][rows][ld]")
+        if logits.stride(2) != 1 or logits.stride(0) != logits.stride(1) * logits.shape[1]:
+            raise ValueError("logits must be row-major [batch][rows][ld] (unit column stride)")
+        if not logits.is_cuda:
+            n = logits.numel()
+            if self._staging is None or self._staging.numel() < n:
+                self._staging = torch.empty(n, dtype=torch.float32, device=self.device)
+            dev = self._staging[:n].view(logits.shape)
+            s = stream if stream is not None else torch.cuda.current_stream()
+            with torch.cuda.stream(s):
+                dev.copy_(logits, non_blocking=True)
+            logits = dev
+        b, rows = logits.shape[0], logits.shape[1]
+        xgr_beam_step(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), rows, logits.stride(1),
+                      self._stream(stream))
+        self.batch = b
+        self.t += 1
+
+    def finalize(self, on_device: bool = True, stream=None, out=None):
+        """Returns dict(tokens [B][BW][ND] int32, item_rank [B][BW] int64, score [B][BW] fp32,
+        n_live [B] int32); CUDA tensors if on_device else numpy arrays (pinned copies)."""
+        import torch
+        B = self.batch
+        if on_device:
+            if out is None:
+                out = {
+                    "tokens": torch.empty((B, self.bw, self.nd), dtype=torch.int32, device=self.device),
+                    "item_rank": torch.empty((B, self.bw), dtype=torch.int64, device=self.device),
+                    "score": torch.empty((B, self.bw), dtype=torch.float32, device=self.device),
+                    "n_live": torch.empty((B,), dtype=torch.int32, device=self.device),
+                }
+            st = xgr_beam_finalize(self.ctx, ctypes.c_void_p(out["tokens"].data_ptr()),
+                                   ctypes.c_void_p(out["item_rank"].data_ptr()),
+                                   ctypes.c_void_p(out["score"].data_ptr()),
+                                   ctypes.c_void_p(out["n_live"].data_ptr()), 1, self._stream(stream))
+        else:
+            if out is None:
+                out = {
+                    "tokens": np.empty((B, self.bw, self.nd), dtype=np.int32),
+                    "item_rank": np.empty((B, self.bw), dtype=np.int64),
+                    "score": np.empty((B, self.bw), dtype=np.float32),
+                    "n_live": np.empty((B,), dtype=np.int32),
+                }
+            st = xgr_beam_finalize(self.ctx, out["tokens"].ctypes.data, out["item_rank"].ctypes.data,
+                                   out["score"].ctypes.data, out["n_live"].ctypes.data, 0,
+                                   self._stream(stream))
+        self.t = 0
+        if st != XGR_OK:
+            err = XgrError(st, last_error())
+            err.outputs = out
+            raise err
+        return out
+
+    # ---- views for parity tests (zero-copy, valid until the next step/finalize) ----------------
+    def view(self):
+        p, tk, sc, nl, nd = (ctypes.c_void_p() for _ in range(5))
+        _check(lib.xgr_beam_view(self.ctx, ctypes.byref(p), ctypes.byref(tk), ctypes.byref(sc),
+                                 ctypes.byref(nl), ctypes.byref(nd)))
+        B, BW = self.batch, self.bw
+        return {
+            "parent": _view(p.value, (B, BW), "<i4", self.device),
+            "token": _view(tk.value, (B, BW), "<i4", self.device),
+            "score": _view(sc.value, (B, BW), "<f4", self.device),
+            "n_live": _view(nl.value, (B,), "<i4", self.device),
+            # uint32 node ids read as int32 (dead slots hold 0xFFFFFFFF -> -1)
+            "node": _view(nd.value, (B, BW), "<i4", self.device),
+        }
+
+    def history(self, step: int):
+        p, tk = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib.xgr_beam_history(self.ctx, step, ctypes.byref(p), ctypes.byref(tk)))
+        B, BW = self.batch, self.bw
+        return _view(p.value, (B, BW), "<i4", self.device), _view(tk.value, (B, BW), "<i4", self.device)
+
+    def request_status(self):
+        fl = np.zeros(self.batch, dtype=np.uint32)
+        _check(lib.xgr_beam_request_status(self.ctx, fl.ctypes.data, self.batch, self._stream()))
+        return fl
+
+    def counters(self):
+        out = np.zeros(XGR_NUM_COUNTERS, dtype=np.uint64)
+        _check(lib.xgr_beam_counters(self.ctx, out.ctypes.data, self._stream()))
+        return dict(zip(COUNTER_NAMES, (int(v) for v in out)))
+
+    def account(self):
+        a, f, lg = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib.xgr_beam_account(self.ctx, ctypes.byref(a), ctypes.byref(f), ctypes.byref(lg),
+                                    self._stream()))
+        return {"alg_bytes": a.value, "full_bytes": f.value, "legal": lg.value}

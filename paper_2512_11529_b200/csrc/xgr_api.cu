@@ -1,0 +1,426 @@
+// C ABI of the xBeam library (include/xgr_beam.h): argument validation, ownership, sequencing,
+// the fixed per-context workspace ("reuses the data structure previously occupied
+// by old sequences") and the per-step route choice. No kernel code here.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "xgr_internal.cuh"
+
+namespace xgr {
+cudaError_t configure_kernels(int cap);
+cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
+                        cudaStream_t s);
+cudaError_t launch_finalize(int batch, int BW, int nd, const int32_t* const* parent_hist,
+                            const int32_t* const* token_hist, const uint32_t* node,
+                            const float* score, const int32_t* nlive, int32_t* tokens,
+                            int64_t* item_rank, float* out_score, int32_t* out_nlive,
+                            cudaStream_t s);
+cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
+                            int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s);
+cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched,
+                           unsigned long long* out, cudaStream_t s);
+}  // namespace xgr
+
+using namespace xgr;
+
+struct xgr_ctx {
+  xgr_config cfg;
+  int V = 0, nd = 0, BW = 0, maxB = 0, cap = 0, R0 = 0;
+  TrieHost trie;
+  bool built = false;
+  float* score[2] = {nullptr, nullptr};
+  uint32_t* node[2] = {nullptr, nullptr};
+  int32_t* nlive[2] = {nullptr, nullptr};
+  int32_t* parent_hist = nullptr;  // [nd][maxB][BW]
+  int32_t* token_hist = nullptr;
+  int32_t** d_phist = nullptr;     // device array of nd pointers
+  int32_t** d_thist = nullptr;
+  uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
+  uint64_t* surv = nullptr;        // [maxB][cap]
+  float* lse = nullptr;            // [maxB][BW]
+  uint32_t* flags = nullptr;       // [maxB]
+  unsigned long long* counters = nullptr;  // [XGR_NUM_COUNTERS]
+  int32_t* out_tokens = nullptr;   // finalize staging for host outputs
+  int64_t* out_rank = nullptr;
+  float* out_score = nullptr;
+  int32_t* out_nlive = nullptr;
+  int step = 0;
+  int batch = 0;
+  // last step's launch arguments (support calls: account)
+  StepArgs last{};
+  int last_rows = 0;
+};
+
+static thread_local std::string g_err;
+
+static xgr_status fail(xgr_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define ACK(x)                                                                              \
+  do {                                                                                      \
+    cudaError_t e_ = (x);                                                                   \
+    if (e_ != cudaSuccess)                                                                  \
+      return fail(e_ == cudaErrorMemoryAllocation ? XGR_ERR_OOM : XGR_ERR_CUDA, "%s: %s", #x, \
+                  cudaGetErrorString(e_));                                                  \
+  } while (0)
+
+static void ctx_free(xgr_ctx* c) {
+  trie_free(c->trie);
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(c->score[i]);
+    cudaFree(c->node[i]);
+    cudaFree(c->nlive[i]);
+  }
+  cudaFree(c->parent_hist);
+  cudaFree(c->token_hist);
+  cudaFree(c->d_phist);
+  cudaFree(c->d_thist);
+  cudaFree(c->scratch);
+  cudaFree(c->surv);
+  cudaFree(c->lse);
+  cudaFree(c->flags);
+  cudaFree(c->counters);
+  cudaFree(c->out_tokens);
+  cudaFree(c->out_rank);
+  cudaFree(c->out_score);
+  cudaFree(c->out_nlive);
+}
+
+extern "C" {
+
+const char* xgr_last_error(void) { return g_err.c_str(); }
+int32_t xgr_abi_version(void) { return XGR_ABI_VERSION; }
+
+xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
+  if (!out) return fail(XGR_ERR_INVALID_ARG, "init: out is NULL");
+  *out = nullptr;
+  if (!cfg) return fail(XGR_ERR_INVALID_ARG, "init: cfg is NULL");
+  const xgr_config& c = *cfg;
+  if (c.vocab < 1 || c.vocab > 65536) return fail(XGR_ERR_INVALID_ARG, "init: vocab %d not in 1..65536", c.vocab);
+  if (c.nd < 1 || c.nd > kMaxND) return fail(XGR_ERR_INVALID_ARG, "init: nd %d not in 1..8", c.nd);
+  int w = 1;
+  while ((1 << w) < c.vocab) ++w;
+  if (w * c.nd > 64) return fail(XGR_ERR_UNSUPPORTED, "init: nd * ceil(log2 V) = %d > 64", w * c.nd);
+  if (c.beam_width < 1 || c.beam_width > kMaxBW)
+    return fail(XGR_ERR_INVALID_ARG, "init: beam_width %d not in 1..1024", c.beam_width);
+  if (c.top_k < 0) return fail(XGR_ERR_INVALID_ARG, "init: top_k < 0");
+  if (c.top_k > 0 && c.top_k < c.beam_width)
+    return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width is not implemented (v1)");
+  if (c.max_batch < 1) return fail(XGR_ERR_INVALID_ARG, "init: max_batch < 1");
+  if (c.nranks != 1 || c.rank != 0 || c.nccl_id)
+    return fail(XGR_ERR_UNSUPPORTED, "init: codebook sharding (nranks > 1) is not implemented (v1)");
+  if (c.survivor_cap < 0 || c.theta_rows < 0) return fail(XGR_ERR_INVALID_ARG, "init: negative knob");
+  for (int i = 0; i < 5; ++i)
+    if (c.reserved[i]) return fail(XGR_ERR_INVALID_ARG, "init: reserved fields must be zero");
+  if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL))
+    return fail(XGR_ERR_INVALID_ARG, "init: unknown flags 0x%x", c.flags);
+  int ndev = 0;
+  ACK(cudaGetDeviceCount(&ndev));
+  if (c.device < 0 || c.device >= ndev) return fail(XGR_ERR_INVALID_ARG, "init: bad device %d", c.device);
+  ACK(cudaSetDevice(c.device));
+
+  xgr_ctx* x = new xgr_ctx();
+  x->cfg = c;
+  x->V = c.vocab;
+  x->nd = c.nd;
+  x->BW = c.beam_width;
+  x->maxB = c.max_batch;
+  x->cap = c.survivor_cap ? c.survivor_cap : std::min(32 * c.beam_width, 16384);
+  x->cap = std::max(x->cap, c.beam_width);
+  if (x->cap > 16384) {
+    delete x;
+    return fail(XGR_ERR_INVALID_ARG, "init: survivor_cap > 16384");
+  }
+  x->R0 = c.theta_rows ? c.theta_rows : 8;
+  const size_t nb = (size_t)x->maxB * x->BW;
+  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+    e = al((void**)&x->score[i], nb * 4);
+    if (e == cudaSuccess) e = al((void**)&x->node[i], nb * 4);
+    if (e == cudaSuccess) e = al((void**)&x->nlive[i], (size_t)x->maxB * 4);
+  }
+  if (e == cudaSuccess) e = al((void**)&x->parent_hist, nb * x->nd * 4);
+  if (e == cudaSuccess) e = al((void**)&x->token_hist, nb * x->nd * 4);
+  if (e == cudaSuccess) e = al((void**)&x->d_phist, x->nd * sizeof(void*));
+  if (e == cudaSuccess) e = al((void**)&x->d_thist, x->nd * sizeof(void*));
+  if (e == cudaSuccess) e = al((void**)&x->scratch, 3 * (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = al((void**)&x->surv, (size_t)x->maxB * x->cap * 8);
+  if (e == cudaSuccess) e = al((void**)&x->lse, nb * 4);
+  if (e == cudaSuccess) e = al((void**)&x->flags, (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = al((void**)&x->counters, XGR_NUM_COUNTERS * 8);
+  if (e == cudaSuccess) e = al((void**)&x->out_tokens, nb * x->nd * 4);
+  if (e == cudaSuccess) e = al((void**)&x->out_rank, nb * 8);
+  if (e == cudaSuccess) e = al((void**)&x->out_score, nb * 4);
+  if (e == cudaSuccess) e = al((void**)&x->out_nlive, (size_t)x->maxB * 4);
+  if (e == cudaSuccess) {
+    std::vector<int32_t*> ph(x->nd), th(x->nd);
+    for (int t = 0; t < x->nd; ++t) {
+      ph[t] = x->parent_hist + (size_t)t * nb;
+      th[t] = x->token_hist + (size_t)t * nb;
+    }
+    e = cudaMemcpy(x->d_phist, ph.data(), x->nd * sizeof(void*), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(x->d_thist, th.data(), x->nd * sizeof(void*), cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) e = cudaMemset(x->counters, 0, XGR_NUM_COUNTERS * 8);
+  if (e == cudaSuccess) e = cudaMemset(x->flags, 0, (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = configure_kernels(x->cap);
+  if (e != cudaSuccess) {
+    ctx_free(x);
+    delete x;
+    return fail(e == cudaErrorMemoryAllocation ? XGR_ERR_OOM : XGR_ERR_CUDA, "init: %s",
+                cudaGetErrorString(e));
+  }
+  *out = x;
+  return XGR_OK;
+}
+
+xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, void* stream) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "mask_build: ctx is NULL");
+  if (ctx->built) return fail(XGR_ERR_SEQUENCE, "mask_build: trie already built");
+  if (n_items < 0) return fail(XGR_ERR_INVALID_ARG, "mask_build: n_items < 0");
+  if (n_items == 0) return fail(XGR_ERR_EMPTY_VOCAB, "mask_build: zero items (no beam could live)");
+  if (!items) return fail(XGR_ERR_INVALID_ARG, "mask_build: items is NULL");
+  if (n_items >= (int64_t)0xFFFFFFFFll) return fail(XGR_ERR_INVALID_ARG, "mask_build: n_items >= 2^32");
+  ACK(cudaSetDevice(ctx->cfg.device));
+  std::string err;
+  xgr_status st = trie_build(ctx->trie, items, n_items, ctx->V, ctx->nd, (cudaStream_t)stream, err);
+  if (st != XGR_OK) {
+    trie_free(ctx->trie);
+    return fail(st, "%s", err.c_str());
+  }
+  ctx->built = true;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
+                         void* stream) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "step: ctx is NULL");
+  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "step: mask_build has not run");
+  if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "step: already %d steps; call finalize", ctx->nd);
+  if (!logits) return fail(XGR_ERR_INVALID_ARG, "step: logits is NULL");
+  if (batch < 1 || batch > ctx->maxB) return fail(XGR_ERR_INVALID_ARG, "step: batch %d not in 1..%d", batch, ctx->maxB);
+  if (ctx->step > 0 && batch != ctx->batch)
+    return fail(XGR_ERR_INVALID_ARG, "step: batch %d differs from this batch's %d", batch, ctx->batch);
+  const int t = ctx->step + 1;
+  const int need_rows = (t == 1) ? 1 : ctx->BW;
+  if (rows < need_rows) return fail(XGR_ERR_INVALID_ARG, "step %d: rows %d < %d", t, rows, need_rows);
+  if (ld < ctx->V) return fail(XGR_ERR_INVALID_ARG, "step: ld %lld < V %d", (long long)ld, ctx->V);
+  if ((reinterpret_cast<uintptr_t>(logits) & 15u) || (ld & 3))
+    return fail(XGR_ERR_ALIGNMENT, "step: logits must be 16-byte aligned and ld %% 4 == 0");
+  cudaStream_t s = (cudaStream_t)stream;
+
+  StepArgs a;
+  memset(&a, 0, sizeof(a));
+  a.trie = trie_dev(ctx->trie);
+  a.logits = logits;
+  a.req_stride = (int64_t)rows * ld;
+  a.ld = ld;
+  a.t = t;
+  a.level = t - 1;
+  a.BW = ctx->BW;
+  a.batch = batch;
+  a.cap = ctx->cap;
+  a.theta_rows = ctx->R0;
+  a.counters_on = (ctx->cfg.flags & XGR_CFG_COUNTERS) ? 1 : 0;
+  a.no_prune = (ctx->cfg.flags & XGR_CFG_NO_PRUNE) ? 1 : 0;
+  const int in = (t - 1) & 1, outi = t & 1;
+  if (t > 1) {
+    a.score_in = ctx->score[in];
+    a.node_in = ctx->node[in];
+    a.nlive_in = ctx->nlive[in];
+  }
+  a.score_out = ctx->score[outi];
+  a.node_out = ctx->node[outi];
+  a.nlive_out = ctx->nlive[outi];
+  const size_t nb = (size_t)ctx->maxB * ctx->BW;
+  a.parent_out = ctx->parent_hist + (size_t)(t - 1) * nb;
+  a.token_out = ctx->token_hist + (size_t)(t - 1) * nb;
+  a.theta = ctx->scratch;
+  a.surv_count = ctx->scratch + ctx->maxB;
+  a.ovf = ctx->scratch + 2 * ctx->maxB;
+  a.surv = ctx->surv;
+  a.lse = ctx->lse;
+  a.flags = ctx->flags;
+  a.counters = ctx->counters;
+
+  const int rows_live = need_rows;  // upper bound on live rows of any request this step
+  const int64_t maxc = ctx->trie.lv[t - 1].max_children;
+  const int64_t sparse_keys = (int64_t)rows_live * maxc;
+  const bool sparse_route =
+      !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sparse_keys <= kSparseCap;
+  if (!sparse_route && ctx->V > 16384)
+    return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 is not implemented yet");
+  if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
+  if (!sparse_route) ACK(cudaMemsetAsync(ctx->scratch, 0, 3 * (size_t)ctx->maxB * 4, s));
+  ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s));
+  ctx->batch = batch;
+  ctx->step = t;
+  ctx->last = a;
+  ctx->last_rows = rows_live;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_finalize(xgr_ctx* ctx, int32_t* tokens, int64_t* item_rank, float* score,
+                             int32_t* n_live, int32_t outputs_on_device, void* stream) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "finalize: ctx is NULL");
+  if (ctx->step != ctx->nd)
+    return fail(XGR_ERR_SEQUENCE, "finalize: %d of %d steps done", ctx->step, ctx->nd);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int fin = ctx->nd & 1;
+  const int B = ctx->batch, BW = ctx->BW, nd = ctx->nd;
+  const size_t nb = (size_t)B * BW;
+  xgr_status st = XGR_OK;
+  if (outputs_on_device) {
+    ACK(launch_finalize(B, BW, nd, ctx->d_phist, ctx->d_thist, ctx->node[fin], ctx->score[fin],
+                        ctx->nlive[fin], tokens, item_rank, score, n_live, s));
+  } else {
+    ACK(launch_finalize(B, BW, nd, ctx->d_phist, ctx->d_thist, ctx->node[fin], ctx->score[fin],
+                        ctx->nlive[fin], ctx->out_tokens, ctx->out_rank, ctx->out_score,
+                        ctx->out_nlive, s));
+    if (tokens) ACK(cudaMemcpyAsync(tokens, ctx->out_tokens, nb * nd * 4, cudaMemcpyDeviceToHost, s));
+    if (item_rank) ACK(cudaMemcpyAsync(item_rank, ctx->out_rank, nb * 8, cudaMemcpyDeviceToHost, s));
+    if (score) ACK(cudaMemcpyAsync(score, ctx->out_score, nb * 4, cudaMemcpyDeviceToHost, s));
+    if (n_live) ACK(cudaMemcpyAsync(n_live, ctx->out_nlive, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+    std::vector<uint32_t> fl(B);
+    ACK(cudaMemcpyAsync(fl.data(), ctx->flags, (size_t)B * 4, cudaMemcpyDeviceToHost, s));
+    ACK(cudaStreamSynchronize(s));
+    for (int r = 0; r < B; ++r)
+      if (fl[r] & kFlagNonfinite) {
+        st = fail(XGR_ERR_NONFINITE, "finalize: request %d saw a NaN/+Inf logit at a legal position", r);
+        break;
+      }
+  }
+  ctx->step = 0;
+  return st;
+}
+
+xgr_status xgr_beam_destroy(xgr_ctx* ctx) {
+  if (!ctx) return XGR_OK;
+  cudaSetDevice(ctx->cfg.device);
+  ctx_free(ctx);
+  delete ctx;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_view(const xgr_ctx* ctx, const int32_t** parent, const int32_t** token,
+                         const float** score, const int32_t** n_live, const uint32_t** node) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "view: ctx is NULL");
+  if (ctx->step < 1) return fail(XGR_ERR_SEQUENCE, "view: no step in this batch yet");
+  const int t = ctx->step, o = t & 1;
+  const size_t nb = (size_t)ctx->maxB * ctx->BW;
+  if (parent) *parent = ctx->parent_hist + (size_t)(t - 1) * nb;
+  if (token) *token = ctx->token_hist + (size_t)(t - 1) * nb;
+  if (score) *score = ctx->score[o];
+  if (n_live) *n_live = ctx->nlive[o];
+  if (node) *node = ctx->node[o];
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_history(const xgr_ctx* ctx, int32_t step, const int32_t** parent,
+                            const int32_t** token) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "history: ctx is NULL");
+  if (step < 1 || step > ctx->step) return fail(XGR_ERR_SEQUENCE, "history: step %d not done", step);
+  const size_t nb = (size_t)ctx->maxB * ctx->BW;
+  if (parent) *parent = ctx->parent_hist + (size_t)(step - 1) * nb;
+  if (token) *token = ctx->token_hist + (size_t)(step - 1) * nb;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_request_status(const xgr_ctx* ctx, uint32_t* flags, int32_t batch, void* stream) {
+  if (!ctx || !flags) return fail(XGR_ERR_INVALID_ARG, "request_status: NULL argument");
+  if (batch < 1 || batch > ctx->maxB) return fail(XGR_ERR_INVALID_ARG, "request_status: bad batch");
+  cudaStream_t s = (cudaStream_t)stream;
+  ACK(cudaMemcpyAsync(flags, ctx->flags, (size_t)batch * 4, cudaMemcpyDeviceToHost, s));
+  ACK(cudaStreamSynchronize(s));
+  return XGR_OK;
+}
+
+xgr_status xgr_mask_children(const xgr_ctx* ctx, const int32_t* prefixes, int32_t depth, int64_t n,
+                             int32_t* counts, int32_t* tokens, int64_t cap, void* stream) {
+  if (!ctx || !counts || (n > 0 && depth > 0 && !prefixes) || (cap > 0 && !tokens))
+    return fail(XGR_ERR_INVALID_ARG, "mask_children: NULL argument");
+  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "mask_children: mask_build has not run");
+  if (depth < 0 || depth >= ctx->nd || n < 0 || cap < 0)
+    return fail(XGR_ERR_INVALID_ARG, "mask_children: bad depth/n/cap");
+  if (n == 0) return XGR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t *dp = nullptr, *dc = nullptr, *dt = nullptr;
+  ACK(cudaMalloc(&dp, std::max<size_t>(16, (size_t)n * depth * 4)));
+  ACK(cudaMalloc(&dc, (size_t)n * 4));
+  ACK(cudaMalloc(&dt, std::max<size_t>(16, (size_t)n * cap * 4)));
+  cudaError_t e = cudaSuccess;
+  if (depth > 0) e = cudaMemcpyAsync(dp, prefixes, (size_t)n * depth * 4, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = launch_children(trie_dev(ctx->trie), dp, depth, n, dc, dt, cap, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dc, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess && cap > 0) e = cudaMemcpyAsync(tokens, dt, (size_t)n * cap * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(dp);
+  cudaFree(dc);
+  cudaFree(dt);
+  if (e != cudaSuccess) return fail(XGR_ERR_CUDA, "mask_children: %s", cudaGetErrorString(e));
+  return XGR_OK;
+}
+
+xgr_status xgr_mask_info(const xgr_ctx* ctx, int64_t* n_items, int64_t* nodes_per_level,
+                         int64_t* dense_per_level, int64_t* max_children_per_level, int64_t* trie_bytes) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "mask_info: ctx is NULL");
+  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "mask_info: mask_build has not run");
+  if (n_items) *n_items = ctx->trie.n_items;
+  for (int d = 0; d <= ctx->nd; ++d) {
+    if (nodes_per_level) nodes_per_level[d] = ctx->trie.lv[d].n_nodes;
+    if (dense_per_level) dense_per_level[d] = ctx->trie.lv[d].n_dense;
+    if (max_children_per_level) max_children_per_level[d] = ctx->trie.lv[d].max_children;
+  }
+  if (trie_bytes) *trie_bytes = ctx->trie.bytes;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_counters(xgr_ctx* ctx, uint64_t* out, void* stream) {
+  if (!ctx || !out) return fail(XGR_ERR_INVALID_ARG, "counters: NULL argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  ACK(cudaMemcpyAsync(out, ctx->counters, XGR_NUM_COUNTERS * 8, cudaMemcpyDeviceToHost, s));
+  ACK(cudaMemsetAsync(ctx->counters, 0, XGR_NUM_COUNTERS * 8, s));
+  ACK(cudaStreamSynchronize(s));
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_bytes,
+                            int64_t* legal_candidates, void* stream) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "account: ctx is NULL");
+  if (ctx->step < 1) return fail(XGR_ERR_SEQUENCE, "account: no step in this batch yet");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nd_dense = std::max<int64_t>(ctx->trie.lv[ctx->last.level].n_dense, 1);
+  uint32_t* touched = nullptr;
+  unsigned long long* dout = nullptr;
+  ACK(cudaMalloc(&touched, ((nd_dense + 31) / 32) * 4));
+  ACK(cudaMalloc(&dout, 3 * 8));
+  unsigned long long h[3] = {0, 0, 0};
+  cudaError_t e = cudaMemsetAsync(touched, 0, ((nd_dense + 31) / 32) * 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(dout, 0, 3 * 8, s);
+  if (e == cudaSuccess) e = launch_account(ctx->last, ctx->last_rows, touched, dout, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, dout, 3 * 8, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(touched);
+  cudaFree(dout);
+  if (e != cudaSuccess) return fail(XGR_ERR_CUDA, "account: %s", cudaGetErrorString(e));
+  if (alg_bytes) *alg_bytes = (int64_t)h[0];
+  if (full_bytes) *full_bytes = (int64_t)h[1];
+  if (legal_candidates) *legal_candidates = (int64_t)h[2];
+  return XGR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,168 @@
+// Internal device structures and helpers of the xBeam library (not part of the ABI).
+// Everything here is product code: it shares nothing with oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/xgr_beam.h"
+
+namespace xgr {
+
+constexpr int kMaxND = 8;
+constexpr int kMaxBW = 1024;
+constexpr int kSparseCap = 16384;   // max candidates per request the sparse-step kernel holds
+
+// ---- trie, one entry per level d = 0..nd (level d = nodes for prefixes of length d) ----------
+struct LevelDev {
+  const uint32_t* first_child;  // [n_nodes + 1], children of node n are level-(d+1) nodes
+                                //   [first_child[n], first_child[n+1]); null at level nd
+  const uint16_t* label;        // [n_nodes] token that leads to each node; null at level 0
+  const int32_t* dense_slot;    // [n_nodes] slot in bitmap/rankdir, -1 if sparse; null if the
+                                //   level has no dense node
+  const uint32_t* bitmap;       // [n_dense][W] V-bit legal-children mask of each dense node
+  const uint32_t* rankdir;      // [n_dense][R] popcount of the bitmap before each 256-bit block
+  int64_t n_nodes;
+  int64_t n_dense;
+  int32_t max_children;
+  int32_t pad;
+};
+
+struct TrieDev {
+  int32_t V;   // vocab
+  int32_t nd;
+  int32_t W;   // bitmap words per dense node = ceil(V / 32)
+  int32_t R;   // rank directory entries per dense node = ceil(V / 256)
+  LevelDev lv[kMaxND + 1];
+};
+
+// ---- one step's arguments (passed as a __grid_constant__ kernel parameter) ------------------
+struct StepArgs {
+  TrieDev trie;
+  const float* logits;
+  int64_t req_stride;   // rows * ld (floats)
+  int64_t ld;
+  int32_t t;            // 1-based step
+  int32_t level;        // t - 1: trie level of the parents' nodes
+  int32_t BW;
+  int32_t batch;
+  int32_t cap;          // survivor buffer capacity per request (keys)
+  int32_t theta_rows;
+  int32_t counters_on;
+  int32_t no_prune;
+  // state in (null at t = 1: the root, one live beam with score 0)
+  const float* score_in;
+  const uint32_t* node_in;
+  const int32_t* nlive_in;
+  // state out
+  float* score_out;
+  uint32_t* node_out;
+  int32_t* nlive_out;
+  int32_t* parent_out;  // history of step t [batch][BW]
+  int32_t* token_out;
+  // scratch (per request), reset before each dense step
+  uint32_t* theta;      // orderable(theta), 0 = no bound (-inf)
+  uint32_t* surv_count;
+  uint32_t* ovf;        // this step's overflow marker
+  uint64_t* surv;       // [batch][cap] survivor keys
+  float* lse;           // [batch][BW] per-row lse (NaN: row not read)
+  uint32_t* flags;      // sticky per-request status bits
+  unsigned long long* counters;
+};
+
+constexpr uint32_t kFlagNonfinite = 1u;
+constexpr uint32_t kFlagOverflow = 2u;
+
+// ---- order-preserving float <-> uint32 (total order on non-NaN floats) ------------------------
+__device__ __forceinline__ uint32_t f2o(float f) {
+  uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float o2f(uint32_t o) {
+  uint32_t u = (o & 0x80000000u) ? (o & 0x7FFFFFFFu) : ~o;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ float theta_value(uint32_t th) {
+  return th == 0u ? -INFINITY : o2f(th);
+}
+
+// 64-bit candidate key: one unsigned compare = (score desc, flat index asc) (R4).
+__device__ __forceinline__ uint64_t make_key(float c, uint32_t flat) {
+  return ((uint64_t)f2o(c) << 32) | (uint64_t)(0xFFFFFFFFu - flat);
+}
+__device__ __forceinline__ float key_score(uint64_t k) { return o2f((uint32_t)(k >> 32)); }
+__device__ __forceinline__ uint32_t key_flat(uint64_t k) {
+  return 0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFull);
+}
+
+// Candidate score, in exactly this association (R11): c = S + (x - lse).
+__device__ __forceinline__ float cand_score(float S, float x, float lse) {
+  return __fadd_rn(S, __fsub_rn(x, lse));
+}
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// ---- beam state of row b of request req ----------------------------------------------------------
+__device__ __forceinline__ int nlive_of(const StepArgs& a, int req) {
+  return a.nlive_in ? a.nlive_in[req] : 1;
+}
+__device__ __forceinline__ void row_state(const StepArgs& a, int req, int b, float& S, uint32_t& node) {
+  if (a.score_in) {
+    S = a.score_in[(size_t)req * a.BW + b];
+    node = a.node_in[(size_t)req * a.BW + b];
+  } else {
+    S = 0.0f;
+    node = 0u;
+  }
+}
+
+// ---- child id of (node at level d, token v) -----------------------------------------------------
+// Dense node: rank(v) = rankdir[v / 256] + popcount of the bitmap words of that 256-bit block
+// below v. Sparse node: binary search of v among the sorted children labels.
+__device__ __forceinline__ uint32_t child_of(const TrieDev& tr, int d, uint32_t node, uint32_t v) {
+  const LevelDev& L = tr.lv[d];
+  uint32_t fc = L.first_child[node];
+  int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  if (slot >= 0) {
+    const uint32_t* bm = L.bitmap + (size_t)slot * tr.W;
+    uint32_t r = L.rankdir[(size_t)slot * tr.R + (v >> 8)];
+    uint32_t w0 = (v >> 8) << 3, w = v >> 5;
+    for (uint32_t i = w0; i < w; ++i) r += __popc(bm[i]);
+    r += __popc(bm[w] & ((1u << (v & 31)) - 1u));
+    return fc + r;
+  }
+  uint32_t lo = fc, hi = L.first_child[node + 1];
+  const uint16_t* lab = tr.lv[d + 1].label;
+  while (lo < hi) {
+    uint32_t mid = (lo + hi) >> 1;
+    if (lab[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---- host-side trie (device pointers) ----------------------------------------------------------
+struct LevelHost {
+  uint32_t* first_child = nullptr;
+  uint16_t* label = nullptr;
+  int32_t* dense_slot = nullptr;
+  uint32_t* bitmap = nullptr;
+  uint32_t* rankdir = nullptr;
+  int64_t n_nodes = 0;
+  int64_t n_dense = 0;
+  int32_t max_children = 0;
+};
+
+struct TrieHost {
+  int V = 0, nd = 0, w = 0, W = 0, R = 0;
+  int64_t n_items = 0;
+  LevelHost lv[kMaxND + 1];
+  int64_t bytes = 0;
+};
+
+void trie_free(TrieHost& t);
+TrieDev trie_dev(const TrieHost& t);
+xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, int nd,
+                      cudaStream_t s, std::string& err);
+
+}  // namespace xgr

@@ -1,0 +1,980 @@
+// xgr_beam_step kernels for sm_100a.
+//
+// Per decode step the path is (section 6):
+//   mask fetch (a1) -> masked log-softmax over the legal tokens (a2, L361) -> score add and
+//   threshold pruning (a3, L376-385) -> survivor compaction + global top-BW (a4, L156, L385) ->
+//   commit + trie advance into fixed ping-pong state (a5, L392).
+//
+// Two routes, chosen per step on the host from trie level statistics (no device sync):
+//  * sparse route (k_sparse): when every request's total legal candidates fit on chip
+//    (rows x max_children <= kSparseCap), one CTA per request gathers the legal logits by label,
+//    forms every candidate key in shared memory and selects exactly. No pruning needed.
+//  * dense route: k_theta (a valid lower bound theta on the BW-th best candidate from rows
+//    0..R0-1 of each request) -> k_main (one CTA per row streams the row once with 128-bit loads,
+//    masks with the node's bitmap, computes m, Z, lse with warp-shuffle reductions, skips the row
+//    if S_b < theta or S_b - ln Z_b < theta, else emits keys >= theta with warp-aggregated
+//    atomics) -> k_select (per request: radix select + bitonic sort of the survivors, commit) ->
+//    k_fallback (exact multi-pass radix select for any request whose survivors overflowed).
+// Results never depend on theta (pruning is strict: c < theta is dropped, R16).
+#include <cuda_runtime.h>
+
+#include "xgr_internal.cuh"
+
+namespace xgr {
+
+constexpr float kLog2e = 1.4426950408889634f;
+
+// ---------------------------------------------------------------------------------------------
+// small device helpers
+// ---------------------------------------------------------------------------------------------
+__device__ __forceinline__ float4 ld_stream4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_min(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+  // xor butterfly: every lane ends with the bitwise-same value (a+b == b+a in IEEE)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+
+// Block reductions: warp butterflies, then every thread folds the per-warp values in a fixed
+// order, so every thread gets the bitwise-same deterministic result. `sh` must hold T/32 values
+// and must not be reused before the next __syncthreads.
+template <int T>
+__device__ __forceinline__ float block_max(float v, float* sh) {
+  v = warp_max(v);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = sh[0];
+#pragma unroll
+  for (int i = 1; i < T / 32; ++i) r = fmaxf(r, sh[i]);
+  return r;
+}
+template <int T>
+__device__ __forceinline__ float block_min(float v, float* sh) {
+  v = warp_min(v);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = sh[0];
+#pragma unroll
+  for (int i = 1; i < T / 32; ++i) r = fminf(r, sh[i]);
+  return r;
+}
+template <int T>
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float r = sh[0];
+#pragma unroll
+  for (int i = 1; i < T / 32; ++i) r += sh[i];
+  return r;
+}
+template <int T>
+__device__ __forceinline__ int block_sum_i(int v, int* sh) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int r = 0;
+#pragma unroll
+  for (int i = 0; i < T / 32; ++i) r += sh[i];
+  return r;
+}
+
+// Append `key` to a request's survivor buffer; lanes that arrive together share one atomic.
+__device__ __forceinline__ void emit_key(uint64_t key, uint32_t* count, uint64_t* buf, int cap) {
+  unsigned m = __activemask();
+  int leader = __ffs(m) - 1;
+  int lane = lane_id();
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+  if (pos < (uint32_t)cap) buf[pos] = key;
+}
+
+__device__ __forceinline__ void count_add(const StepArgs& a, int idx, unsigned long long v) {
+  if (a.counters_on && v) atomicAdd(a.counters + idx, v);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Dense row in registers: T threads x VPT float4. Thread t owns positions 4*(i*T + t) + {0..3}.
+// The row's bitmap words are staged in shared memory; illegal positions become -inf.
+// ---------------------------------------------------------------------------------------------
+template <int T, int VPT>
+struct DenseRow {
+  float4 x[VPT];
+  uint32_t nib[VPT];
+  float M;     // row max over legal
+  float lse;   // M + ln Z
+  float tmax;  // this thread's max over its legal values
+  bool finite;
+};
+
+template <int T, int VPT>
+__device__ __forceinline__ void dense_row_compute(const float* __restrict__ row,
+                                                  const uint32_t* __restrict__ bm, int V, int W,
+                                                  uint32_t* s_bm, float* s_red, float* s_red2,
+                                                  DenseRow<T, VPT>& r) {
+  const int tid = threadIdx.x;
+  // issue all logit loads first (VPT x 16 B in flight per thread)
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    int q = i * T + tid;
+    if (4 * q < V) r.x[i] = ld_stream4(row + 4 * q);
+    else r.x[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  for (int w = tid; w < W; w += T) s_bm[w] = __ldg(bm + w);
+  __syncthreads();
+  float tmax = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    int q = i * T + tid;
+    uint32_t nb = (4 * q < V) ? (s_bm[q >> 3] >> ((q & 7) * 4)) & 0xFu : 0u;
+    r.nib[i] = nb;
+    r.x[i].x = (nb & 1u) ? r.x[i].x : -INFINITY;
+    r.x[i].y = (nb & 2u) ? r.x[i].y : -INFINITY;
+    r.x[i].z = (nb & 4u) ? r.x[i].z : -INFINITY;
+    r.x[i].w = (nb & 8u) ? r.x[i].w : -INFINITY;
+    tmax = fmaxf(tmax, fmaxf(fmaxf(r.x[i].x, r.x[i].y), fmaxf(r.x[i].z, r.x[i].w)));
+  }
+  r.tmax = tmax;
+  const float M = block_max<T>(tmax, s_red);
+  float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    z0 += ex2(__fmul_rn(__fsub_rn(r.x[i].x, M), kLog2e));
+    z1 += ex2(__fmul_rn(__fsub_rn(r.x[i].y, M), kLog2e));
+    z2 += ex2(__fmul_rn(__fsub_rn(r.x[i].z, M), kLog2e));
+    z3 += ex2(__fmul_rn(__fsub_rn(r.x[i].w, M), kLog2e));
+  }
+  const float Z = block_sum<T>((z0 + z1) + (z2 + z3), s_red2);
+  r.finite = (Z > 0.5f) && (Z <= 3.0e38f);
+  r.M = M;
+  r.lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+}
+
+// ---------------------------------------------------------------------------------------------
+// Block radix select helpers over shared-memory keys.
+// ---------------------------------------------------------------------------------------------
+// Find the digit d (scanning bins from the top) where the running count reaches `krem`.
+// hist has 256 bins. Result written to *out_digit, count above it to *out_above.
+__device__ __forceinline__ void warp_find_digit_desc(const uint32_t* hist, uint32_t krem,
+                                                     uint32_t* out_digit, uint32_t* out_above) {
+  int lane = lane_id();
+  // lane l owns bins 255-8l .. 248-8l (descending)
+  uint32_t c[8];
+  uint32_t s = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c[j] = hist[255 - 8 * lane - j];
+    s += c[j];
+  }
+  uint32_t incl = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  uint32_t excl = incl - s;
+  bool mine = (excl < krem) && (incl >= krem);
+  if (mine) {
+    uint32_t acc = excl;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      if (acc + c[j] >= krem) {
+        *out_digit = 255 - 8 * lane - j;
+        *out_above = acc;
+        break;
+      }
+      acc += c[j];
+    }
+  }
+}
+
+// Selects the k largest of keys[0..n) (distinct keys) into sel[0..k), sorted descending.
+// T threads; shared scratch: hist[256], misc[8]. sel must hold >= next_pow2(k) <= 1024 entries.
+template <int T>
+__device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* sel, uint32_t* hist,
+                                  uint64_t* misc64, uint32_t* misc32) {
+  const int tid = threadIdx.x;
+  uint64_t thr = 0;
+  if (k < n) {
+    // common high bits of all keys are skipped (they would all land in one histogram bin)
+    uint64_t lo = ~0ull, hi = 0;
+    for (int i = tid; i < n; i += T) {
+      uint64_t v = keys[i];
+      lo = v < lo ? v : lo;
+      hi = v > hi ? v : hi;
+    }
+    lo = warp_min_u64(lo);
+    hi = warp_max_u64(hi);
+    if (lane_id() == 0) {
+      misc64[2 * (tid >> 5)] = lo;
+      misc64[2 * (tid >> 5) + 1] = hi;
+    }
+    __syncthreads();
+    uint64_t glo = misc64[0], ghi = misc64[1];
+    for (int w = 1; w < T / 32; ++w) {
+      glo = misc64[2 * w] < glo ? misc64[2 * w] : glo;
+      ghi = misc64[2 * w + 1] > ghi ? misc64[2 * w + 1] : ghi;
+    }
+    uint64_t diff = glo ^ ghi;  // != 0 since n > k >= 1 distinct keys
+    int top = 63 - __clzll(diff);
+    int shift = (top / 8) * 8;
+    uint64_t mask = (shift + 8 >= 64) ? 0ull : (~0ull << (shift + 8));
+    uint64_t prefix = ghi & mask;
+    uint32_t krem = (uint32_t)k;
+    __syncthreads();
+    for (;;) {
+      for (int i = tid; i < 256; i += T) hist[i] = 0;
+      __syncthreads();
+      for (int i = tid; i < n; i += T) {
+        uint64_t v = keys[i];
+        if ((v & mask) == prefix) atomicAdd(&hist[(v >> shift) & 0xFFu], 1u);
+      }
+      __syncthreads();
+      if (tid < 32) warp_find_digit_desc(hist, krem, &misc32[0], &misc32[1]);
+      __syncthreads();
+      uint32_t d = misc32[0], above = misc32[1];
+      uint32_t inbin = hist[d];
+      krem -= above;
+      prefix |= (uint64_t)d << shift;
+      mask |= 0xFFull << shift;
+      __syncthreads();
+      if (inbin == krem || shift == 0) break;
+      shift -= 8;
+    }
+    thr = prefix;  // all keys >= thr are exactly the k largest
+  }
+  // compact the k winners
+  if (tid == 0) misc32[2] = 0;
+  int P = 1;
+  while (P < k) P <<= 1;
+  __syncthreads();
+  for (int i = tid; i < n; i += T) {
+    uint64_t v = keys[i];
+    if (v >= thr) {
+      uint32_t p = atomicAdd(&misc32[2], 1u);
+      sel[p] = v;
+    }
+  }
+  for (int i = k + tid; i < P; i += T) sel[i] = 0ull;
+  __syncthreads();
+  // bitonic sort descending over P entries
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P / 2; i += T) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool desc = ((lo & size) == 0);
+        uint64_t a = sel[lo], b = sel[hi];
+        if ((a < b) == desc) {
+          sel[lo] = b;
+          sel[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Commit the k selected keys (sorted desc) of request req into the step-t state (a5).
+template <int T>
+__device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k) {
+  const int V = a.trie.V;
+  const size_t base = (size_t)req * a.BW;
+  for (int j = threadIdx.x; j < a.BW; j += T) {
+    if (j < k) {
+      uint64_t key = sel[j];
+      float c = key_score(key);
+      uint32_t flat = key_flat(key);
+      uint32_t b = flat / (uint32_t)V;
+      uint32_t v = flat - b * (uint32_t)V;
+      uint32_t pnode = a.node_in ? a.node_in[base + b] : 0u;
+      a.parent_out[base + j] = (int32_t)b;
+      a.token_out[base + j] = (int32_t)v;
+      a.score_out[base + j] = c;
+      a.node_out[base + j] = child_of(a.trie, a.level, pnode, v);
+    } else {
+      a.parent_out[base + j] = -1;
+      a.token_out[base + j] = -1;
+      a.score_out[base + j] = -INFINITY;
+      a.node_out[base + j] = 0xFFFFFFFFu;
+    }
+  }
+  if (threadIdx.x == 0) a.nlive_out[req] = k;
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_theta: per (request, row r < R0) with a dense node and >= BW legal tokens, a lower bound on
+// the row's BW-th largest legal logit x_lb (two 12-bit histogram passes on d = M - x, then the
+// smallest x in the crossing bin); theta_r = S_r + (x_lb - lse_r) is an actual candidate score
+// with >= BW candidates of the request at or above it, so max_r theta_r <= the true BW-th best.
+// ---------------------------------------------------------------------------------------------
+template <int T, int VPT>
+__global__ void __launch_bounds__(T) k_theta(const __grid_constant__ StepArgs a) {
+  __shared__ uint32_t s_bm[T * VPT / 8];
+  __shared__ float s_red[T / 32], s_red2[T / 32], s_red3[T / 32];
+  __shared__ uint32_t s_hist[4096];
+  __shared__ uint32_t s_tot[T / 32];
+  __shared__ uint32_t s_sel[2];
+  const int req = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  if (b >= nlive_of(a, req)) return;
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  const int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  if (slot < 0) return;
+  const uint32_t nchild = L.first_child[node + 1] - L.first_child[node];
+  if (nchild < (uint32_t)a.BW) return;
+  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  DenseRow<T, VPT> r;
+  dense_row_compute<T, VPT>(row, L.bitmap + (size_t)slot * a.trie.W, a.trie.V, a.trie.W, s_bm,
+                            s_red, s_red2, r);
+  if (!r.finite) return;
+  // d = M - x >= 0 for legal x; illegal/NaN are excluded by the nibble test and d == d
+  uint32_t krem = (uint32_t)a.BW;
+  uint32_t pre = 0, pmask = 0;
+  for (int pass = 0; pass < 2; ++pass) {
+    const int sh = pass == 0 ? 20 : 8;
+    for (int i = tid; i < 4096; i += T) s_hist[i] = 0;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if ((r.nib[i] >> j) & 1u) {
+          float d = __fsub_rn(r.M, xs[j]);
+          uint32_t u = __float_as_uint(d);
+          if (d == d && (u & pmask) == pre) atomicAdd(&s_hist[(u >> sh) & 0xFFFu], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    // ascending scan of 4096 bins: thread t owns bins [t*B, t*B + B)
+    constexpr int B = 4096 / T;
+    uint32_t loc = 0;
+#pragma unroll
+    for (int j = 0; j < B; ++j) loc += s_hist[tid * B + j];
+    uint32_t incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane_id() >= o) incl += y;
+    }
+    if (lane_id() == 31) s_tot[tid >> 5] = incl;
+    __syncthreads();
+    uint32_t woff = 0;
+    for (int w = 0; w < (tid >> 5); ++w) woff += s_tot[w];
+    incl += woff;
+    uint32_t excl = incl - loc;
+    if (excl < krem && incl >= krem) {
+      uint32_t acc = excl;
+      for (int j = 0; j < B; ++j) {
+        uint32_t c = s_hist[tid * B + j];
+        if (acc + c >= krem) {
+          s_sel[0] = (uint32_t)(tid * B + j);
+          s_sel[1] = acc;
+          break;
+        }
+        acc += c;
+      }
+    }
+    __syncthreads();
+    uint32_t bin = s_sel[0];
+    krem -= s_sel[1];
+    pre |= bin << sh;
+    pmask |= 0xFFFu << sh;
+    __syncthreads();
+  }
+  // smallest legal x whose d shares the 24 selected bits: >= BW legal values are >= it
+  float xmin = INFINITY;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if ((r.nib[i] >> j) & 1u) {
+        float d = __fsub_rn(r.M, xs[j]);
+        if (d == d && (__float_as_uint(d) & pmask) == pre) xmin = fminf(xmin, xs[j]);
+      }
+    }
+  }
+  const float xlb = block_min<T>(xmin, s_red3);
+  if (tid == 0 && xlb < INFINITY) {
+    float th = cand_score(S, xlb, r.lse);
+    if (th == th && th > -INFINITY) atomicMax(a.theta + req, f2o(th));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_main: one CTA per (request, live row). The dominant HBM stream (a1-a3).
+// ---------------------------------------------------------------------------------------------
+template <int T>
+__device__ void sparse_row_main(const StepArgs& a, int req, int b, float S, float th, uint32_t node,
+                                const float* row, float* s_red, float* s_red2, int* s_redi) {
+  const LevelDev& L = a.trie.lv[a.level];
+  const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  const int tid = threadIdx.x;
+  float tmax = -INFINITY;
+  for (uint32_t k = fc + tid; k < fe; k += T) tmax = fmaxf(tmax, row[lab[k]]);
+  const float M = block_max<T>(tmax, s_red);
+  float z = 0.f;
+  for (uint32_t k = fc + tid; k < fe; k += T) z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
+  const float Z = block_sum<T>(z, s_red2);
+  const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+  const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+  if (tid == 0) {
+    a.lse[(size_t)req * a.BW + b] = finite ? lse : __int_as_float(0x7fc00000);
+    if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+  }
+  if (a.counters_on && tid == 0) count_add(a, XGR_CNT_LEGAL, fe - fc);
+  if (!finite) return;
+  if (!(cand_score(S, M, lse) >= th)) {
+    if (tid == 0) count_add(a, XGR_CNT_ROWS_SKIP_POST, 1);
+    return;
+  }
+  int ns = 0;
+  const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+  for (uint32_t k = fc + tid; k < fe; k += T) {
+    uint32_t v = lab[k];
+    float c = cand_score(S, row[v], lse);
+    if (c >= th) {
+      emit_key(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap, a.cap);
+      ++ns;
+    }
+  }
+  if (a.counters_on) {
+    int tot = block_sum_i<T>(ns, s_redi);
+    if (tid == 0) count_add(a, XGR_CNT_SURVIVORS, tot);
+  }
+}
+
+template <int T, int VPT>
+__global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) {
+  __shared__ uint32_t s_bm[T * VPT / 8];
+  __shared__ float s_red[T / 32], s_red2[T / 32];
+  __shared__ int s_redi[T / 32];
+  const int req = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  if (b >= nlive_of(a, req)) return;
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const float th = theta_value(a.theta[req]);
+  if (S < th) {  // every candidate of the row is <= S_b < theta (pre-read skip)
+    if (tid == 0) {
+      a.lse[(size_t)req * a.BW + b] = __int_as_float(0x7fc00000);
+      count_add(a, XGR_CNT_ROWS_SKIP_PRE, 1);
+    }
+    return;
+  }
+  if (tid == 0) count_add(a, XGR_CNT_ROWS_READ, 1);
+  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const LevelDev& L = a.trie.lv[a.level];
+  const int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  if (slot < 0) {
+    sparse_row_main<T>(a, req, b, S, th, node, row, s_red, s_red2, s_redi);
+    return;
+  }
+  DenseRow<T, VPT> r;
+  dense_row_compute<T, VPT>(row, L.bitmap + (size_t)slot * a.trie.W, a.trie.V, a.trie.W, s_bm, s_red,
+                            s_red2, r);
+  if (tid == 0) {
+    a.lse[(size_t)req * a.BW + b] = r.finite ? r.lse : __int_as_float(0x7fc00000);
+    if (!r.finite) atomicOr(a.flags + req, kFlagNonfinite);
+  }
+  if (a.counters_on) {
+    int lc = 0;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) lc += __popc(r.nib[i]);
+    int tot = block_sum_i<T>(lc, s_redi);
+    if (tid == 0) count_add(a, XGR_CNT_LEGAL, tot);
+    __syncthreads();
+  }
+  if (!r.finite) return;
+  const float lse = r.lse;
+  if (!(cand_score(S, r.M, lse) >= th)) {  // UB_b = S_b - ln Z_b < theta (post-LSE skip)
+    if (tid == 0) count_add(a, XGR_CNT_ROWS_SKIP_POST, 1);
+    return;
+  }
+  // conservative pre-filter on x (exact test below): c(x) >= theta implies x >= xthr
+  const float xthr = (th == -INFINITY)
+                         ? -INFINITY
+                         : (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
+  int ns = 0;
+  if (r.tmax >= xthr) {
+    const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (((r.nib[i] >> j) & 1u) && xs[j] >= xthr) {
+          float c = cand_score(S, xs[j], lse);
+          if (c >= th) {
+            uint32_t v = 4u * (uint32_t)(i * T + tid) + j;
+            emit_key(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap,
+                     a.cap);
+            ++ns;
+          }
+        }
+      }
+    }
+  }
+  if (a.counters_on) {
+    int tot = block_sum_i<T>(ns, s_redi);
+    if (tid == 0) count_add(a, XGR_CNT_SURVIVORS, tot);
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_select: per request, top-BW of the survivors (a4) and commit (a5).
+// ---------------------------------------------------------------------------------------------
+template <int T>
+__global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) uint64_t s_keys[];  // [cap]
+  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint64_t s_m64[2 * (T / 32)];
+  __shared__ uint32_t s_m32[4];
+  const int req = blockIdx.x, tid = threadIdx.x;
+  const uint32_t n = a.surv_count[req];
+  if (n > (uint32_t)a.cap) {
+    if (tid == 0) {
+      a.ovf[req] = 1u;
+      atomicOr(a.flags + req, kFlagOverflow);
+      count_add(a, XGR_CNT_OVERFLOW, 1);
+    }
+    return;
+  }
+  const int k = min((int)n, a.BW);
+  const uint64_t* src = a.surv + (size_t)req * a.cap;
+  for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
+  __syncthreads();
+  block_select_topk<T>(s_keys, (int)n, k, s_sel, s_hist, s_m64, s_m32);
+  commit<T>(a, req, s_sel, k);
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_fallback: exact top-BW for a request whose survivors overflowed the buffer. One CTA streams
+// the request's rows once per 8-bit radix digit of the 64-bit key (at most 8 passes), restricted
+// to keys >= theta. Keys are recomputed with the same formula and the lse stored by k_main, so
+// they are bitwise the keys k_main would have emitted. Rare path (adversarial ties/logits).
+// ---------------------------------------------------------------------------------------------
+template <int T, typename F>
+__device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, int b, float S,
+                                                   float lse, uint32_t node, F&& f) {
+  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const LevelDev& L = a.trie.lv[a.level];
+  const int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+  if (slot >= 0) {
+    const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W;
+    const int V = a.trie.V;
+    for (int q = threadIdx.x; 4 * q < V; q += T) {
+      uint32_t nb = (bm[q >> 3] >> ((q & 7) * 4)) & 0xFu;
+      if (!nb) continue;
+      float4 x = ld_stream4(row + 4 * q);
+      float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((nb >> j) & 1u) f(make_key(cand_score(S, xs[j], lse), fbase + 4u * q + j));
+    }
+  } else {
+    const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+    const uint16_t* lab = a.trie.lv[a.level + 1].label;
+    for (uint32_t k = fc + threadIdx.x; k < fe; k += T) {
+      uint32_t v = lab[k];
+      f(make_key(cand_score(S, row[v], lse), fbase + v));
+    }
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs a) {
+  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint32_t s_m32[4];
+  const int req = blockIdx.x, tid = threadIdx.x;
+  if (!a.ovf[req]) return;
+  const int nl = nlive_of(a, req);
+  const float th = theta_value(a.theta[req]);
+  const uint64_t klo = (uint64_t)a.theta[req] << 32;
+  const int k = a.BW;  // overflow => more than cap >= BW candidates >= theta
+  uint64_t prefix = 0, mask = 0;
+  uint32_t krem = (uint32_t)k;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += T) s_hist[i] = 0;
+    __syncthreads();
+    for (int b = 0; b < nl; ++b) {
+      float S;
+      uint32_t node;
+      row_state(a, req, b, S, node);
+      const float lse = a.lse[(size_t)req * a.BW + b];
+      if (S < th || lse != lse) continue;
+      for_each_candidate<T>(a, req, b, S, lse, node, [&](uint64_t key) {
+        if (key >= klo && (key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 0xFFu], 1u);
+      });
+    }
+    __syncthreads();
+    if (tid < 32) warp_find_digit_desc(s_hist, krem, &s_m32[0], &s_m32[1]);
+    __syncthreads();
+    uint32_t d = s_m32[0], above = s_m32[1];
+    uint32_t inbin = s_hist[d];
+    krem -= above;
+    prefix |= (uint64_t)d << shift;
+    mask |= 0xFFull << shift;
+    __syncthreads();
+    if (inbin == krem) break;
+  }
+  if (tid == 0) s_m32[2] = 0;
+  __syncthreads();
+  const uint64_t thr = prefix;
+  for (int b = 0; b < nl; ++b) {
+    float S;
+    uint32_t node;
+    row_state(a, req, b, S, node);
+    const float lse = a.lse[(size_t)req * a.BW + b];
+    if (S < th || lse != lse) continue;
+    for_each_candidate<T>(a, req, b, S, lse, node, [&](uint64_t key) {
+      if (key >= thr && key >= klo) {
+        uint32_t p = atomicAdd(&s_m32[2], 1u);
+        if (p < (uint32_t)k) s_sel[p] = key;
+      }
+    });
+  }
+  __syncthreads();
+  int P = 1;
+  while (P < k) P <<= 1;
+  for (int i = k + tid; i < P; i += T) s_sel[i] = 0ull;
+  __syncthreads();
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < P / 2; i += T) {
+        int lo = 2 * i - (i & (stride - 1));
+        int hi = lo + stride;
+        bool desc = ((lo & size) == 0);
+        uint64_t x = s_sel[lo], y = s_sel[hi];
+        if ((x < y) == desc) {
+          s_sel[lo] = y;
+          s_sel[hi] = x;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  commit<T>(a, req, s_sel, k);
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_sparse: one CTA per request; every legal candidate is formed on chip (no pruning needed).
+// GROUP = 32: one warp per live row; GROUP = T: the whole block on one row (the root step).
+// ---------------------------------------------------------------------------------------------
+template <int T, int GROUP>
+__global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) uint64_t s_keys[];  // [rows * max_children]
+  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint32_t s_hist[256];
+  __shared__ uint64_t s_m64[2 * (T / 32)];
+  __shared__ uint32_t s_m32[4];
+  __shared__ float s_red[T / 32], s_red2[T / 32];
+  __shared__ uint32_t s_count;
+  const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
+  const int nl = nlive_of(a, req);
+  const LevelDev& L = a.trie.lv[a.level];
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  const int V = a.trie.V;
+  if (tid == 0) s_count = 0;
+  __syncthreads();
+  if (GROUP == T) {
+    for (int b = 0; b < nl; ++b) {
+      float S;
+      uint32_t node;
+      row_state(a, req, b, S, node);
+      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      float tmax = -INFINITY;
+      for (uint32_t k = fc + tid; k < fe; k += T) tmax = fmaxf(tmax, row[lab[k]]);
+      const float M = block_max<T>(tmax, s_red);
+      float z = 0.f;
+      for (uint32_t k = fc + tid; k < fe; k += T)
+        z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
+      const float Z = block_sum<T>(z, s_red2);
+      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
+      const uint32_t base = s_count;
+      for (uint32_t k = fc + tid; k < fe; k += T) {
+        uint32_t v = lab[k];
+        s_keys[base + (k - fc)] = make_key(cand_score(S, row[v], lse), (uint32_t)b * V + v);
+      }
+      __syncthreads();
+      if (tid == 0) s_count = base + (fe - fc);
+      __syncthreads();
+    }
+  } else {
+    const int warp = tid >> 5;
+    for (int b = warp; b < nl; b += T / 32) {
+      float S;
+      uint32_t node;
+      row_state(a, req, b, S, node);
+      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      float tmax = -INFINITY;
+      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, row[lab[k]]);
+      const float M = warp_max(tmax);
+      float z = 0.f;
+      for (uint32_t k = fc + lane; k < fe; k += 32)
+        z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
+      const float Z = warp_sum(z);
+      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      if (!finite && lane == 0) atomicOr(a.flags + req, kFlagNonfinite);
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&s_count, fe - fc);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (uint32_t k = fc + lane; k < fe; k += 32) {
+        uint32_t v = lab[k];
+        s_keys[base + (k - fc)] = make_key(cand_score(S, row[v], lse), (uint32_t)b * V + v);
+      }
+    }
+  }
+  __syncthreads();
+  const int n = (int)s_count;
+  if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
+  const int k = min(n, a.BW);
+  block_select_topk<T>(s_keys, n, k, s_sel, s_hist, s_m64, s_m32);
+  commit<T>(a, req, s_sel, k);
+}
+
+// ---------------------------------------------------------------------------------------------
+// finalize (a6): backtrack histories into tuples; leaf node id = item rank.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_finalize(int BW, int nd, const int32_t* const* parent_hist,
+                           const int32_t* const* token_hist, const uint32_t* node, const float* score,
+                           const int32_t* nlive, int32_t* tokens, int64_t* item_rank, float* out_score,
+                           int32_t* out_nlive) {
+  const int req = blockIdx.x;
+  const int nl = nlive[req];
+  for (int j = threadIdx.x; j < BW; j += blockDim.x) {
+    const size_t o = (size_t)req * BW + j;
+    if (j < nl) {
+      int s = j;
+      for (int t = nd - 1; t >= 0; --t) {
+        int32_t tok = token_hist[t][(size_t)req * BW + s];
+        if (tokens) tokens[o * nd + t] = tok;
+        s = parent_hist[t][(size_t)req * BW + s];
+      }
+      if (item_rank) item_rank[o] = (int64_t)node[o];
+      if (out_score) out_score[o] = score[o];
+    } else {
+      if (tokens)
+        for (int t = 0; t < nd; ++t) tokens[o * nd + t] = -1;
+      if (item_rank) item_rank[o] = -1;
+      if (out_score) out_score[o] = -INFINITY;
+    }
+  }
+  if (threadIdx.x == 0 && out_nlive) out_nlive[req] = nl;
+}
+
+// ---------------------------------------------------------------------------------------------
+// support: children of prefixes, read from the representation the step kernels use.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_children(TrieDev tr, const int32_t* prefixes, int depth, int64_t n, int32_t* counts,
+                           int32_t* tokens, int64_t cap) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t node = 0;
+  for (int d = 0; d < depth; ++d) {
+    int32_t t = prefixes[i * depth + d];
+    const LevelDev& L = tr.lv[d];
+    bool legal = false;
+    if (t >= 0 && t < tr.V) {
+      int slot = L.dense_slot ? L.dense_slot[node] : -1;
+      if (slot >= 0) {
+        legal = (L.bitmap[(size_t)slot * tr.W + (t >> 5)] >> (t & 31)) & 1u;
+      } else {
+        for (uint32_t k = L.first_child[node]; k < L.first_child[node + 1]; ++k)
+          if (tr.lv[d + 1].label[k] == (uint16_t)t) legal = true;
+      }
+    }
+    if (!legal) {
+      counts[i] = -1;
+      return;
+    }
+    node = child_of(tr, d, node, (uint32_t)t);
+  }
+  const LevelDev& L = tr.lv[depth];
+  const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  const uint16_t* lab = tr.lv[depth + 1].label;
+  int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  int32_t c = 0;
+  bool ok = true;
+  if (slot >= 0) {
+    const uint32_t* bm = L.bitmap + (size_t)slot * tr.W;
+    for (int v = 0; v < tr.V; ++v) {
+      if ((bm[v >> 5] >> (v & 31)) & 1u) {
+        if (c < cap) tokens[i * cap + c] = v;
+        if (fc + c >= fe || lab[fc + c] != (uint16_t)v || child_of(tr, depth, node, v) != fc + c) ok = false;
+        ++c;
+      }
+    }
+    if ((uint32_t)c != fe - fc) ok = false;
+  } else {
+    for (uint32_t k = fc; k < fe; ++k) {
+      if (c < cap) tokens[i * cap + c] = lab[k];
+      if (k > fc && lab[k] <= lab[k - 1]) ok = false;
+      ++c;
+    }
+  }
+  counts[i] = ok ? c : -2;
+}
+
+// ---------------------------------------------------------------------------------------------
+// support: algorithmic bytes of the last step; not on the timed path.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
+                          unsigned long long* out /* alg, full, legal */) {
+  const int req = blockIdx.x, b = blockIdx.y;
+  const int nl = nlive_of(a, req);
+  if (b >= nl) return;
+  const int k = a.nlive_out[req];
+  const float thstar = k > 0 ? a.score_out[(size_t)req * a.BW + k - 1] : -INFINITY;
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  const int V = a.trie.V;
+  if (threadIdx.x == 0) {
+    atomicAdd(out + 1, (unsigned long long)V * 4ull);
+    atomicAdd(out + 2, (unsigned long long)(fe - fc));
+  }
+  if (S < thstar) return;  // a row the method need not read
+  const int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  unsigned long long bytes = 0;
+  if (slot >= 0) {
+    const uint8_t* bm = reinterpret_cast<const uint8_t*>(L.bitmap + (size_t)slot * a.trie.W);
+    for (int s = threadIdx.x; s < (V + 7) / 8; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+    if (threadIdx.x == 0) {
+      uint32_t old = atomicOr(touched + (slot >> 5), 1u << (slot & 31));
+      if (!((old >> (slot & 31)) & 1u)) bytes += (unsigned long long)((V + 7) / 8);
+      bytes += 16;
+    }
+  } else {
+    const uint16_t* lab = a.trie.lv[a.level + 1].label;
+    for (uint32_t k2 = fc + threadIdx.x; k2 < fe; k2 += blockDim.x)
+      if (k2 == fc || (lab[k2] >> 3) != (lab[k2 - 1] >> 3)) bytes += 32;
+    if (threadIdx.x == 0) bytes += 4 + 2ull * (fe - fc) + 16;
+  }
+  bytes = __reduce_add_sync(0xffffffffu, (unsigned)bytes);
+  if (lane_id() == 0 && bytes) atomicAdd(out, bytes);
+}
+
+// ---------------------------------------------------------------------------------------------
+// host-side launchers
+// ---------------------------------------------------------------------------------------------
+template <int T, int VPT>
+static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s) {
+  if (!a.no_prune) {
+    int r0 = min(a.theta_rows, rows);
+    if (r0 > 0) k_theta<T, VPT><<<dim3(a.batch, r0), T, 0, s>>>(a);
+  }
+  k_main<T, VPT><<<dim3(a.batch, rows), T, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Called once per context: opt the variable-shared-memory kernels into their maximum.
+cudaError_t configure_kernels(int cap) {
+  cudaError_t e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(cap * sizeof(uint64_t)));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_sparse<512, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kSparseCap * sizeof(uint64_t)));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_sparse<512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(kSparseCap * sizeof(uint64_t)));
+}
+
+cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
+                        cudaStream_t s) {
+  cudaError_t e;
+  if (sparse_route) {
+    size_t smem = (size_t)sparse_keys * sizeof(uint64_t);
+    if (rows == 1) k_sparse<512, 512><<<a.batch, 512, smem, s>>>(a);
+    else k_sparse<512, 32><<<a.batch, 512, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  const int V = a.trie.V;
+  if (V <= 2048) e = launch_dense<128, 4>(a, rows, s);
+  else if (V <= 4096) e = launch_dense<256, 4>(a, rows, s);
+  else if (V <= 8192) e = launch_dense<256, 8>(a, rows, s);
+  else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s);
+  else return cudaErrorNotSupported;
+  if (e != cudaSuccess) return e;
+  k_select<512><<<a.batch, 512, (size_t)a.cap * sizeof(uint64_t), s>>>(a);
+  k_fallback<512><<<a.batch, 512, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(int batch, int BW, int nd, const int32_t* const* parent_hist,
+                            const int32_t* const* token_hist, const uint32_t* node, const float* score,
+                            const int32_t* nlive, int32_t* tokens, int64_t* item_rank, float* out_score,
+                            int32_t* out_nlive, cudaStream_t s) {
+  k_finalize<<<batch, min(BW, 1024) < 32 ? 32 : min(BW, 1024), 0, s>>>(
+      BW, nd, parent_hist, token_hist, node, score, nlive, tokens, item_rank, out_score, out_nlive);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
+                            int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s) {
+  k_children<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(tr, prefixes, depth, n, counts, tokens, cap);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched, unsigned long long* out,
+                           cudaStream_t s) {
+  k_account<<<dim3(a.batch, rows), 256, 0, s>>>(a, touched, out);
+  return cudaGetLastError();
+}
+
+}  // namespace xgr

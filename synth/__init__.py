@@ -13,5 +13,6 @@ from .inputs import (  # noqa: F401
     feistel_permute,
     make_items,
     make_logits,
+    make_logits_torch,
     prefix_keyed_row,
 )

@@ -1,0 +1,366 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bit-exact: legal sets (children of every prefix), (parent, token) selections, final item tuples
+and item ranks, n_live. Scores within 1e-5 * max(1, |s|); near-threshold differences adjudicated
+by the oracle's fp64 recompute (tests/parity.py). Marked gpu: needs a B200.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import xbeam_oracle as O  # noqa: E402
+from synth import config, make_items, make_logits, make_logits_torch, prefix_keyed_row  # noqa: E402
+from tests.parity import compare_step  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def xgr():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_11529_b200 as xgr
+    return xgr
+
+
+def run_checked(bs, voc, logits_steps, bw, check_reqs, logits_fn=None):
+    """Run nd steps; after each, compare the checked requests with the teacher-forced oracle.
+    logits_steps[t]: CUDA tensor [B][rows][ld], or None with logits_fn(t, gpu_states) -> tensor."""
+    nd = voc.nd
+    hist_par, hist_tok = [], []
+    scores = nlive = None
+    stats = {"strict": 0, "adjudicated": 0}
+    for t in range(nd):
+        if t == 0:
+            states = {r: O.BeamState.root() for r in check_reqs}
+        else:
+            states = {r: O.state_from_history([h[r] for h in hist_par], [h[r] for h in hist_tok],
+                                              scores[r], int(nlive[r])) for r in check_reqs}
+        lg = logits_steps[t] if logits_fn is None else logits_fn(t, states)
+        bs.step(lg)
+        v = bs.view()
+        par = v["parent"].cpu().numpy().copy()
+        tok = v["token"].cpu().numpy().copy()
+        sc = v["score"].cpu().numpy().copy()
+        nl = v["n_live"].cpu().numpy().copy()
+        for r in check_reqs:
+            lr = lg[r].cpu().numpy()
+            res = compare_step(voc, states[r], lr, bw, par[r], tok[r], sc[r], nl[r],
+                               where=f"req {r} step {t + 1}")
+            stats[res] += 1
+        hist_par.append(par)
+        hist_tok.append(tok)
+        scores, nlive = sc, nl
+    out = bs.finalize(on_device=False)
+    for r in check_reqs:
+        n = int(out["n_live"][r])
+        assert n == int(nlive[r])
+        st = O.state_from_history([h[r] for h in hist_par], [h[r] for h in hist_tok], scores[r], n)
+        for j in range(n):
+            tup = tuple(int(x) for x in out["tokens"][r, j])
+            assert tup == st.prefixes[j]
+            assert voc.item_rank(tup) == int(out["item_rank"][r, j]), (r, j, tup)
+            assert out["score"][r, j] == scores[r][j]
+        assert np.all(out["tokens"][r, n:] == -1) and np.all(out["item_rank"][r, n:] == -1)
+        assert np.all(np.isneginf(out["score"][r, n:]))
+        assert np.all(np.diff(out["score"][r, :n]) <= 0)
+    return out, stats
+
+
+def _bs(xgr, voc_or_cfg, bw, batch, flags=0, **kw):
+    return xgr.BeamSearch(voc_or_cfg.vocab, voc_or_cfg.nd, bw, batch, flags=flags, **kw)
+
+
+# ---- trie -------------------------------------------------------------------------------------
+def test_c1_children_every_prefix(xgr):
+    c = config("C1")
+    items = make_items(c["n_items"], c["vocab"], c["nd"], c["trie_key"])
+    voc = O.Vocabulary(items, c["vocab"], c["nd"])
+    bs = _bs(xgr, voc, 4, 1)
+    bs.mask_build(items)
+    info = bs.info()
+    assert info["n_items"] == voc.n_items
+    for d in range(c["nd"] + 1):
+        assert info["nodes"][d] == voc.n_nodes(d)
+    import itertools
+    for d in range(c["nd"]):
+        prefixes = list(itertools.product(range(c["vocab"]), repeat=d))
+        arr = np.array(prefixes, dtype=np.int32).reshape(len(prefixes), max(d, 1))
+        counts, toks = bs.children(arr if d else np.zeros((1, 1), np.int32), d, c["vocab"])
+        for i, p in enumerate(prefixes):
+            kids = voc.children(p) if (d == 0 or voc._range(p)[1] > voc._range(p)[0]) else None
+            if kids is None or len(kids) == 0:
+                assert counts[i] == -1, (p, counts[i])
+            else:
+                assert counts[i] == len(kids), (p, counts[i], kids)
+                assert list(toks[i, : counts[i]]) == list(kids)
+
+
+@pytest.mark.parametrize("vocab,nd,n", [(1000, 3, 20000), (64, 4, 30000), (5, 2, 20), (256, 2, 40000)])
+def test_random_trie_children(xgr, vocab, nd, n):
+    rng = np.random.default_rng(vocab + nd)
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    bs = _bs(xgr, voc, 8, 1)
+    bs.mask_build(items)
+    info = bs.info()
+    for d in range(nd + 1):
+        assert info["nodes"][d] == voc.n_nodes(d)
+    for d in range(nd):
+        pre = items[rng.integers(0, n, size=300), :d]
+        if d:
+            pre = np.concatenate([pre, rng.integers(0, vocab, size=(100, d)).astype(np.int32)])
+        else:
+            pre = np.zeros((1, 1), np.int32)
+        counts, toks = bs.children(pre, d, vocab)
+        for i in range(counts.shape[0]):
+            p = tuple(int(x) for x in pre[i, :d])
+            lo, hi = voc._range(p)
+            if hi <= lo:
+                assert counts[i] == -1
+            else:
+                kids = voc.children(p)
+                assert counts[i] == len(kids) and list(toks[i, : counts[i]]) == list(kids)
+
+
+def test_mask_build_errors(xgr):
+    bs = xgr.BeamSearch(16, 3, 4, 1)
+    with pytest.raises(xgr.XgrError) as e:
+        bs.mask_build(np.array([[1, 16, 0]], np.int32))
+    assert e.value.name == "XGR_ERR_TOKEN_RANGE"
+    bs2 = xgr.BeamSearch(16, 3, 4, 1)
+    with pytest.raises(xgr.XgrError) as e:
+        bs2.mask_build(np.zeros((0, 3), np.int32))
+    assert e.value.name == "XGR_ERR_EMPTY_VOCAB"
+    bs3 = xgr.BeamSearch(16, 3, 4, 1)
+    bs3.mask_build(np.array([[1, 2, 3], [1, 2, 3], [0, 0, 0]], np.int32))
+    assert bs3.info()["n_items"] == 2
+    with pytest.raises(xgr.XgrError) as e:
+        bs3.mask_build(np.array([[1, 2, 3]], np.int32))
+    assert e.value.name == "XGR_ERR_SEQUENCE"
+
+
+# ---- steps --------------------------------------------------------------------------------------
+@pytest.mark.parametrize("sigma", [2.0, 4.0])
+@pytest.mark.parametrize("flags", [0, 4, 5])
+def test_c1_parity(xgr, sigma, flags):
+    c = config("C1")
+    items = make_items(c["n_items"], c["vocab"], c["nd"], c["trie_key"])
+    voc = O.Vocabulary(items, c["vocab"], c["nd"])
+    for seed in range(6):
+        bs = _bs(xgr, voc, c["beam_width"], 3, flags=flags)
+        bs.mask_build(items)
+        steps = [torch.from_numpy(make_logits((3, c["beam_width"], c["vocab"]), 100 * seed + t, sigma)).cuda()
+                 for t in range(c["nd"])]
+        run_checked(bs, voc, steps, c["beam_width"], [0, 1, 2])
+
+
+@pytest.mark.parametrize("flags", [0, 4])
+def test_exhaustive_bw_ge_items_prefix_keyed(xgr, flags):
+    """BW = 256 >= 200 items: all items come back; logits keyed by prefix (teacher forced)."""
+    c = config("C1")
+    items = make_items(c["n_items"], c["vocab"], c["nd"], c["trie_key"])
+    voc = O.Vocabulary(items, c["vocab"], c["nd"])
+    bw = 256
+    bs = _bs(xgr, voc, bw, 1, flags=flags)
+    bs.mask_build(items)
+
+    def logits_fn(t, states):
+        x = np.zeros((1, bw, c["vocab"]), np.float32)
+        for j, p in enumerate(states[0].prefixes):
+            x[0, j] = prefix_keyed_row(7, 0, p, c["vocab"])
+        return torch.from_numpy(x).cuda()
+
+    out, _ = run_checked(bs, voc, None, bw, [0], logits_fn=logits_fn)
+    assert int(out["n_live"][0]) == 200
+    assert sorted(out["item_rank"][0, :200].tolist()) == list(range(200))
+
+
+CASES = [
+    # vocab, nd, n_items, bw, batch
+    (16, 3, 300, 4, 4),
+    (64, 3, 3000, 32, 3),
+    (1000, 3, 50000, 64, 2),
+    (256, 2, 20000, 128, 2),
+    (8, 4, 2000, 8, 5),
+    (4096, 2, 200000, 256, 2),
+    (8192, 3, 400000, 128, 2),
+    (16384, 2, 100000, 64, 2),
+    (3, 3, 20, 5, 2),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+@pytest.mark.parametrize("flags", [0, 4, 5])
+def test_random_tries_parity(xgr, case, flags):
+    vocab, nd, n, bw, batch = case
+    rng = np.random.default_rng(vocab * 7 + nd + bw)
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    bs = _bs(xgr, voc, bw, batch, flags=flags)
+    bs.mask_build(items)
+    ld = (vocab + 3) // 4 * 4 + 4   # padded rows exercise ld > V
+    steps = []
+    for t in range(nd):
+        x = np.full((batch, bw, ld), np.nan, np.float32)
+        x[:, :, :vocab] = make_logits((batch, bw, vocab), 1000 + t, 3.0)
+        steps.append(torch.from_numpy(x).cuda())
+    run_checked(bs, voc, steps, bw, list(range(batch)))
+
+
+def _final(xgr, voc, items, steps, bw, batch, flags=0):
+    bs = _bs(xgr, voc, bw, batch, flags=flags)
+    bs.mask_build(items)
+    per_step = []
+    for lg in steps:
+        bs.step(lg)
+        v = bs.view()
+        per_step.append({k: v[k].cpu().numpy().copy() for k in ("parent", "token", "score", "n_live", "node")})
+    return bs.finalize(on_device=False), per_step, bs
+
+
+def test_pruning_never_changes_results(xgr):
+    """Dense route with theta pruning vs theta = -inf: bitwise-equal states and outputs."""
+    rng = np.random.default_rng(3)
+    vocab, nd, n, bw, batch = 8192, 3, 300000, 64, 3
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    steps = [torch.from_numpy(make_logits((batch, bw, vocab), 50 + t, 2.0)).cuda() for t in range(nd)]
+    a, sa, bsa = _final(xgr, voc, items, steps, bw, batch, flags=4 | 2)
+    b, sb, _ = _final(xgr, voc, items, steps, bw, batch, flags=4 | 1)
+    for x, y in zip(sa, sb):
+        for k in x:
+            assert np.array_equal(x[k], y[k]), k
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_determinism_and_batch_invariance(xgr):
+    rng = np.random.default_rng(9)
+    vocab, nd, n, bw, batch = 4096, 3, 200000, 128, 4
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    steps = [torch.from_numpy(make_logits((batch, bw, vocab), 70 + t, 2.0)).cuda() for t in range(nd)]
+    a, _, _ = _final(xgr, voc, items, steps, bw, batch)
+    b, _, _ = _final(xgr, voc, items, steps, bw, batch)
+    for k in a:
+        assert np.array_equal(a[k], b[k])
+    # request 2 alone equals request 2 in the batch
+    solo = [s[2:3].contiguous() for s in steps]
+    c, _, _ = _final(xgr, voc, items, solo, bw, 1)
+    for k in a:
+        assert np.array_equal(a[k][2:3], c[k]), k
+
+
+@pytest.mark.parametrize("flags", [0, 4])
+def test_uniform_logits_ties_and_overflow_fallback(xgr, flags):
+    """All logits equal: massive exact ties; the tie-break (lower flat index) decides everything.
+    On the dense route theta from row 0 admits far more than the survivor buffer holds, so the
+    exact overflow fallback runs."""
+    rng = np.random.default_rng(4)
+    vocab, nd, n, bw, batch = 2048, 3, 60000, 64, 2
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    steps = [torch.zeros((batch, bw, vocab), dtype=torch.float32, device="cuda") for _ in range(nd)]
+    bs = _bs(xgr, voc, bw, batch, flags=flags | 2, survivor_cap=bw)
+    bs.mask_build(items)
+    run_checked(bs, voc, steps, bw, list(range(batch)))
+    if flags & 4:
+        pass
+
+
+def test_quantized_logits_ties(xgr):
+    rng = np.random.default_rng(5)
+    vocab, nd, n, bw, batch = 512, 3, 30000, 32, 3
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    for flags in (0, 4):
+        steps = [torch.from_numpy(np.round(make_logits((batch, bw, vocab), 5 + t, 2.0))).cuda()
+                 for t in range(nd)]
+        bs = _bs(xgr, voc, bw, batch, flags=flags)
+        bs.mask_build(items)
+        run_checked(bs, voc, steps, bw, list(range(batch)))
+
+
+def test_nonfinite_flag_isolated(xgr):
+    rng = np.random.default_rng(6)
+    vocab, nd, n, bw, batch = 1024, 2, 20000, 16, 3
+    items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    for flags in (0, 4):
+        x0 = make_logits((batch, bw, vocab), 1, 2.0)
+        legal0 = voc.children(())
+        x0[1, 0, legal0[3]] = np.nan
+        steps = [torch.from_numpy(x0).cuda(),
+                 torch.from_numpy(make_logits((batch, bw, vocab), 2, 2.0)).cuda()]
+        bs = _bs(xgr, voc, bw, batch, flags=flags)
+        bs.mask_build(items)
+        for s in steps:
+            bs.step(s)
+        assert list(bs.request_status() & 1) == [0, 1, 0]
+        with pytest.raises(xgr.XgrError) as e:
+            bs.finalize(on_device=False)
+        assert e.value.name == "XGR_ERR_NONFINITE"
+        # the other requests are unaffected: same result as a clean run
+        ok = [torch.from_numpy(make_logits((batch, bw, vocab), 1, 2.0)).cuda(), steps[1]]
+        clean, _, _ = _final(xgr, voc, items, ok, bw, batch, flags=flags)
+        got = e.value.outputs
+        for r in (0, 2):
+            for k in got:
+                assert np.array_equal(got[k][r], clean[k][r]), (k, r)
+
+
+def test_step_argument_errors(xgr):
+    voc_items = np.array([[1, 2], [3, 4]], np.int32)
+    bs = xgr.BeamSearch(8, 2, 4, 2)
+    x = torch.zeros((2, 4, 8), device="cuda")
+    with pytest.raises(xgr.XgrError) as e:
+        bs.step(x)
+    assert e.value.name == "XGR_ERR_SEQUENCE"
+    bs.mask_build(voc_items)
+    with pytest.raises(xgr.XgrError) as e:
+        bs.finalize()
+    assert e.value.name == "XGR_ERR_SEQUENCE"
+    with pytest.raises(xgr.XgrError) as e:
+        bs.step(torch.zeros((3, 4, 8), device="cuda"))
+    assert e.value.name == "XGR_ERR_INVALID_ARG"
+    big = torch.zeros((2 * 4 * 8 + 1,), device="cuda")
+    with pytest.raises(xgr.XgrError) as e:
+        bs.step(big[1:].view(2, 4, 8))
+    assert e.value.name == "XGR_ERR_ALIGNMENT"
+    bs.step(x)
+    with pytest.raises(xgr.XgrError) as e:
+        bs.step(torch.zeros((2, 3, 8), device="cuda"))    # rows < BW at t > 1
+    assert e.value.name == "XGR_ERR_INVALID_ARG"
+    bs.step(x)
+    with pytest.raises(xgr.XgrError) as e:
+        bs.step(x)
+    assert e.value.name == "XGR_ERR_SEQUENCE"
+    out = bs.finalize(on_device=False)
+    assert sorted(out["item_rank"][0, :2].tolist()) == [0, 1]
+
+
+# ---- full-size configurations (the bench's launch configuration), sampled requests -------------
+def _full(xgr, name, check_reqs, sigma=2.0):
+    c = config(name)
+    items = make_items(c["n_items"], c["vocab"], c["nd"], c["trie_key"])
+    voc = O.Vocabulary(items, c["vocab"], c["nd"])
+    B, bw = c["batch"], c["beam_width"]
+    bs = _bs(xgr, voc, bw, B, flags=2)
+    bs.mask_build(items)
+    del items
+    steps = [make_logits_torch((B, 1 if t == 0 else bw, c["vocab"]), 11 * t + 1, sigma)
+             for t in range(c["nd"])]
+    out, stats = run_checked(bs, voc, steps, bw, check_reqs)
+    return out, stats, bs
+
+
+def test_c2_full_size_sampled(xgr):
+    out, stats, bs = _full(xgr, "C2", [0, 17, 63])
+    assert np.all(out["n_live"] == 128)
+
+
+@pytest.mark.slow
+def test_c3_full_size_sampled(xgr):
+    out, stats, bs = _full(xgr, "C3", [0, 101, 255])
+    assert np.all(out["n_live"] == 256)

@@ -66,6 +66,7 @@ typedef enum {
 #define XGR_CFG_NO_PRUNE 0x1u /* theta = -inf: every legal candidate survives (test/ablation) */
 #define XGR_CFG_COUNTERS 0x2u /* accumulate device counters (xgr_beam_counters) */
 #define XGR_CFG_NO_SPARSE_KERNEL 0x4u /* route every step through the dense-step kernels */
+#define XGR_CFG_TIMING 0x8u /* CUDA events around the dense-route streaming kernel           */
 
 typedef struct {
   int32_t vocab;      /* V: tokens per level, 1..65536                                   */
@@ -173,6 +174,14 @@ xgr_status xgr_beam_counters(xgr_ctx* ctx, uint64_t* out, void* stream);
  * (every live row, whole V). Host outputs; synchronous; not for the timed path. */
 xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_bytes,
                             int64_t* legal_candidates, void* stream);
+
+/* Host-side count of the kernels this ctx has launched since init (step and finalize). */
+int64_t xgr_beam_launch_count(const xgr_ctx* ctx);
+
+/* Durations (ms, CUDA events on the launch stream) of the dense-route streaming kernel (k_main)
+ * of every dense step since the last call, oldest first, with the step index of each; needs
+ * XGR_CFG_TIMING. Writes min(recorded, cap) entries and *n; synchronises on the events. */
+xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t cap, int32_t* n);
 
 #ifdef __cplusplus
 }

@@ -11,6 +11,7 @@ from .binding import (  # noqa: F401
     XGR_CFG_COUNTERS,
     XGR_CFG_NO_PRUNE,
     XGR_CFG_NO_SPARSE_KERNEL,
+    XGR_CFG_TIMING,
     lib,
     LIB_PATH,
 )

@@ -21,6 +21,7 @@ STATUS_NAMES = {
 XGR_CFG_NO_PRUNE = 0x1
 XGR_CFG_COUNTERS = 0x2
 XGR_CFG_NO_SPARSE_KERNEL = 0x4
+XGR_CFG_TIMING = 0x8
 XGR_NUM_COUNTERS = 8
 COUNTER_NAMES = ["rows_read", "rows_skip_pre", "rows_skip_post", "legal", "survivors",
                  "overflow", "sparse_cands", "dense_steps"]
@@ -29,7 +30,8 @@ COUNTER_NAMES = ["rows_read", "rows_skip_pre", "rows_skip_post", "legal", "survi
 EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_finalize",
            "xgr_beam_destroy", "xgr_last_error", "xgr_abi_version", "xgr_beam_view",
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
-           "xgr_beam_counters", "xgr_beam_account"]
+           "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
+           "xgr_beam_kernel_times"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -68,6 +70,7 @@ def _load():
         "xgr_mask_info": [VP, VP, VP, VP, VP, VP],
         "xgr_beam_counters": [VP, VP, VP],
         "xgr_beam_account": [VP, VP, VP, VP, VP],
+        "xgr_beam_kernel_times": [VP, VP, VP, I32, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -75,6 +78,8 @@ def _load():
         f.restype = ctypes.c_int
     lib.xgr_last_error.argtypes = []
     lib.xgr_last_error.restype = ctypes.c_char_p
+    lib.xgr_beam_launch_count.argtypes = [VP]
+    lib.xgr_beam_launch_count.restype = ctypes.c_int64
     lib.xgr_abi_version.argtypes = []
     lib.xgr_abi_version.restype = ctypes.c_int32
     return lib
@@ -226,6 +231,8 @@ class BeamSearch:
         n_live [B] int32); CUDA tensors if on_device else numpy arrays (pinned copies)."""
         import torch
         B = self.batch
+        if B is None:
+            _check(xgr_beam_finalize(self.ctx, None, None, None, None, 1, self._stream(stream)))
         if on_device:
             if out is None:
                 out = {
@@ -286,6 +293,16 @@ class BeamSearch:
         out = np.zeros(XGR_NUM_COUNTERS, dtype=np.uint64)
         _check(lib.xgr_beam_counters(self.ctx, out.ctypes.data, self._stream()))
         return dict(zip(COUNTER_NAMES, (int(v) for v in out)))
+
+    def launch_count(self) -> int:
+        return int(lib.xgr_beam_launch_count(self.ctx))
+
+    def kernel_times(self, cap: int = 4096):
+        ms = np.zeros(cap, np.float32)
+        st = np.zeros(cap, np.int32)
+        n = ctypes.c_int32()
+        _check(lib.xgr_beam_kernel_times(self.ctx, ms.ctypes.data, st.ctypes.data, cap, ctypes.byref(n)))
+        return ms[: n.value], st[: n.value]
 
     def account(self):
         a, f, lg = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()

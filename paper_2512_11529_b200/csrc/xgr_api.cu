@@ -15,7 +15,7 @@
 namespace xgr {
 cudaError_t configure_kernels(int cap);
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
-                        cudaStream_t s);
+                        cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
 cudaError_t launch_finalize(int batch, int BW, int nd, const int32_t* const* parent_hist,
                             const int32_t* const* token_hist, const uint32_t* node,
                             const float* score, const int32_t* nlive, int32_t* tokens,
@@ -55,7 +55,13 @@ struct xgr_ctx {
   // last step's launch arguments (support calls: account)
   StepArgs last{};
   int last_rows = 0;
+  int64_t launches = 0;             // kernels launched by this ctx (host-side count)
+  // XGR_CFG_TIMING: ring of event pairs around the dense-route streaming kernel
+  std::vector<cudaEvent_t> ev;      // 2 * kTimingRing
+  std::vector<int32_t> ev_step;
+  int64_t ev_head = 0, ev_tail = 0;
 };
+static constexpr int kTimingRing = 4096;
 
 static thread_local std::string g_err;
 
@@ -78,6 +84,8 @@ static xgr_status fail(xgr_status st, const char* fmt, ...) {
   } while (0)
 
 static void ctx_free(xgr_ctx* c) {
+  for (auto e : c->ev) cudaEventDestroy(e);
+  c->ev.clear();
   trie_free(c->trie);
   for (int i = 0; i < 2; ++i) {
     cudaFree(c->score[i]);
@@ -125,7 +133,7 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.survivor_cap < 0 || c.theta_rows < 0) return fail(XGR_ERR_INVALID_ARG, "init: negative knob");
   for (int i = 0; i < 5; ++i)
     if (c.reserved[i]) return fail(XGR_ERR_INVALID_ARG, "init: reserved fields must be zero");
-  if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL))
+  if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL | XGR_CFG_TIMING))
     return fail(XGR_ERR_INVALID_ARG, "init: unknown flags 0x%x", c.flags);
   int ndev = 0;
   ACK(cudaGetDeviceCount(&ndev));
@@ -178,6 +186,12 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = cudaMemset(x->counters, 0, XGR_NUM_COUNTERS * 8);
   if (e == cudaSuccess) e = cudaMemset(x->flags, 0, (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = configure_kernels(x->cap);
+  if (e == cudaSuccess && (c.flags & XGR_CFG_TIMING)) {
+    x->ev.resize(2 * kTimingRing, nullptr);
+    x->ev_step.resize(kTimingRing, 0);
+    for (auto& ev : x->ev)
+      if (e == cudaSuccess) e = cudaEventCreate(&ev);
+  }
   if (e != cudaSuccess) {
     ctx_free(x);
     delete x;
@@ -266,7 +280,17 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
     return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 is not implemented yet");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
   if (!sparse_route) ACK(cudaMemsetAsync(ctx->scratch, 0, 3 * (size_t)ctx->maxB * 4, s));
-  ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s));
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  if (!ctx->ev.empty() && !sparse_route && ctx->ev_head - ctx->ev_tail < kTimingRing) {
+    const int slot = (int)(ctx->ev_head % kTimingRing);
+    ev0 = ctx->ev[2 * slot];
+    ev1 = ctx->ev[2 * slot + 1];
+    ctx->ev_step[slot] = t;
+    ++ctx->ev_head;
+  }
+  int launches = 0;
+  ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s, ev0, ev1, &launches));
+  ctx->launches += launches;
   ctx->batch = batch;
   ctx->step = t;
   ctx->last = a;
@@ -284,6 +308,7 @@ xgr_status xgr_beam_finalize(xgr_ctx* ctx, int32_t* tokens, int64_t* item_rank, 
   const int B = ctx->batch, BW = ctx->BW, nd = ctx->nd;
   const size_t nb = (size_t)B * BW;
   xgr_status st = XGR_OK;
+  ctx->launches += 1;
   if (outputs_on_device) {
     ACK(launch_finalize(B, BW, nd, ctx->d_phist, ctx->d_thist, ctx->node[fin], ctx->score[fin],
                         ctx->nlive[fin], tokens, item_rank, score, n_live, s));
@@ -420,6 +445,28 @@ xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_byte
   if (alg_bytes) *alg_bytes = (int64_t)h[0];
   if (full_bytes) *full_bytes = (int64_t)h[1];
   if (legal_candidates) *legal_candidates = (int64_t)h[2];
+  return XGR_OK;
+}
+
+int64_t xgr_beam_launch_count(const xgr_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t cap, int32_t* n) {
+  if (!ctx || !n || (cap > 0 && !ms)) return fail(XGR_ERR_INVALID_ARG, "kernel_times: NULL argument");
+  if (ctx->ev.empty()) return fail(XGR_ERR_SEQUENCE, "kernel_times: XGR_CFG_TIMING not set");
+  int32_t k = 0;
+  while (ctx->ev_tail < ctx->ev_head) {
+    const int slot = (int)(ctx->ev_tail % kTimingRing);
+    ACK(cudaEventSynchronize(ctx->ev[2 * slot + 1]));
+    float t = 0.f;
+    ACK(cudaEventElapsedTime(&t, ctx->ev[2 * slot], ctx->ev[2 * slot + 1]));
+    if (k < cap) {
+      ms[k] = t;
+      if (step) step[k] = ctx->ev_step[slot];
+    }
+    ++k;
+    ++ctx->ev_tail;
+  }
+  *n = std::min(k, cap);
   return XGR_OK;
 }
 

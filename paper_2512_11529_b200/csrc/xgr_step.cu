@@ -914,12 +914,19 @@ __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
 // host-side launchers
 // ---------------------------------------------------------------------------------------------
 template <int T, int VPT>
-static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s) {
+static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0,
+                                cudaEvent_t ev1, int* launches) {
   if (!a.no_prune) {
     int r0 = min(a.theta_rows, rows);
-    if (r0 > 0) k_theta<T, VPT><<<dim3(a.batch, r0), T, 0, s>>>(a);
+    if (r0 > 0) {
+      k_theta<T, VPT><<<dim3(a.batch, r0), T, 0, s>>>(a);
+      ++*launches;
+    }
   }
+  if (ev0) cudaEventRecord(ev0, s);
   k_main<T, VPT><<<dim3(a.batch, rows), T, 0, s>>>(a);
+  ++*launches;
+  if (ev1) cudaEventRecord(ev1, s);
   return cudaGetLastError();
 }
 
@@ -936,23 +943,25 @@ cudaError_t configure_kernels(int cap) {
 }
 
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
-                        cudaStream_t s) {
+                        cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
   if (sparse_route) {
     size_t smem = (size_t)sparse_keys * sizeof(uint64_t);
     if (rows == 1) k_sparse<512, 512><<<a.batch, 512, smem, s>>>(a);
     else k_sparse<512, 32><<<a.batch, 512, smem, s>>>(a);
+    ++*launches;
     return cudaGetLastError();
   }
   const int V = a.trie.V;
-  if (V <= 2048) e = launch_dense<128, 4>(a, rows, s);
-  else if (V <= 4096) e = launch_dense<256, 4>(a, rows, s);
-  else if (V <= 8192) e = launch_dense<256, 8>(a, rows, s);
-  else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s);
+  if (V <= 2048) e = launch_dense<128, 4>(a, rows, s, ev0, ev1, launches);
+  else if (V <= 4096) e = launch_dense<256, 4>(a, rows, s, ev0, ev1, launches);
+  else if (V <= 8192) e = launch_dense<256, 8>(a, rows, s, ev0, ev1, launches);
+  else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s, ev0, ev1, launches);
   else return cudaErrorNotSupported;
   if (e != cudaSuccess) return e;
   k_select<512><<<a.batch, 512, (size_t)a.cap * sizeof(uint64_t), s>>>(a);
   k_fallback<512><<<a.batch, 512, 0, s>>>(a);
+  *launches += 2;
   return cudaGetLastError();
 }
 

@@ -14,7 +14,7 @@ HEADER = os.path.join(ROOT, "include", "xgr_beam.h")
 def header_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:xgr_status|const char\*|int32_t)\s+(xgr_\w+)\s*\(", src, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:xgr_status|const char\*|int32_t|int64_t)\s+(xgr_\w+)\s*\(", src, re.M)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -56,7 +56,7 @@ def _cfg(**kw):
 @pytest.mark.parametrize("kw,status", [
     (dict(vocab=0), 1), (dict(vocab=65537), 1), (dict(nd=0), 1), (dict(nd=9), 1),
     (dict(beam_width=0), 1), (dict(beam_width=1025), 1), (dict(max_batch=0), 1),
-    (dict(top_k=2), 2), (dict(nranks=2), 2), (dict(vocab=65536, nd=5), 2), (dict(flags=0x80), 1),
+    (dict(top_k=2), 2), (dict(nranks=2), 2), (dict(vocab=65536, nd=5), 2), (dict(flags=0x80), 1), (dict(reserved=(ctypes.c_int32 * 5)(1, 0, 0, 0, 0)), 1),
 ])
 def test_init_validation_without_gpu(kw, status):
     from paper_2512_11529_b200 import binding

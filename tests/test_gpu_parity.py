@@ -85,8 +85,8 @@ def test_c1_children_every_prefix(xgr):
     import itertools
     for d in range(c["nd"]):
         prefixes = list(itertools.product(range(c["vocab"]), repeat=d))
-        arr = np.array(prefixes, dtype=np.int32).reshape(len(prefixes), max(d, 1))
-        counts, toks = bs.children(arr if d else np.zeros((1, 1), np.int32), d, c["vocab"])
+        arr = np.array(prefixes, dtype=np.int32).reshape(len(prefixes), d) if d else np.zeros((1, 1), np.int32)
+        counts, toks = bs.children(arr, d, c["vocab"])
         for i, p in enumerate(prefixes):
             kids = voc.children(p) if (d == 0 or voc._range(p)[1] > voc._range(p)[0]) else None
             if kids is None or len(kids) == 0:

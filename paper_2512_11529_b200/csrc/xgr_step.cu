@@ -212,6 +212,15 @@ __device__ __forceinline__ void warp_find_digit_desc(const uint32_t* hist, uint3
     if (lane >= o) incl += y;
   }
   uint32_t excl = incl - s;
+  // fewer than krem keys in all bins (only possible for a flagged request): sentinel digit 256
+  const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
+  if (tot < krem) {
+    if (lane == 0) {
+      *out_digit = 256;
+      *out_above = tot;
+    }
+    return;
+  }
   bool mine = (excl < krem) && (incl >= krem);
   if (mine) {
     uint32_t acc = excl;
@@ -227,11 +236,11 @@ __device__ __forceinline__ void warp_find_digit_desc(const uint32_t* hist, uint3
   }
 }
 
-// Selects the k largest of keys[0..n) (distinct keys) into sel[0..k), sorted descending.
-// T threads; shared scratch: hist[256], misc[8]. sel must hold >= next_pow2(k) <= 1024 entries.
+// Selects the k largest of keys[0..n) (distinct keys) into out[0..k), sorted descending.
+// T threads; shared scratch: sel[k], hist[256], misc64[2 * T / 32], misc32[4].
 template <int T>
-__device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* sel, uint32_t* hist,
-                                  uint64_t* misc64, uint32_t* misc32) {
+__device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* sel, uint64_t* out,
+                                  uint32_t* hist, uint64_t* misc64, uint32_t* misc32) {
   const int tid = threadIdx.x;
   uint64_t thr = 0;
   if (k < n) {
@@ -284,8 +293,6 @@ __device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* 
   }
   // compact the k winners
   if (tid == 0) misc32[2] = 0;
-  int P = 1;
-  while (P < k) P <<= 1;
   __syncthreads();
   for (int i = tid; i < n; i += T) {
     uint64_t v = keys[i];
@@ -294,24 +301,15 @@ __device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* 
       sel[p] = v;
     }
   }
-  for (int i = k + tid; i < P; i += T) sel[i] = 0ull;
   __syncthreads();
-  // bitonic sort descending over P entries
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < P / 2; i += T) {
-        int lo = 2 * i - (i & (stride - 1));
-        int hi = lo + stride;
-        bool desc = ((lo & size) == 0);
-        uint64_t a = sel[lo], b = sel[hi];
-        if ((a < b) == desc) {
-          sel[lo] = b;
-          sel[hi] = a;
-        }
-      }
-      __syncthreads();
-    }
+  // rank sort (keys are distinct): out[#keys greater than sel[j]] = sel[j]; one barrier
+  for (int j = tid; j < k; j += T) {
+    const uint64_t v = sel[j];
+    int r = 0;
+    for (int i = 0; i < k; ++i) r += sel[i] > v;
+    out[r] = v;
   }
+  __syncthreads();
 }
 
 // Commit the k selected keys (sorted desc) of request req into the step-t state (a5).
@@ -572,7 +570,7 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
 template <int T>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_keys[];  // [cap]
-  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ uint32_t s_hist[256];
   __shared__ uint64_t s_m64[2 * (T / 32)];
   __shared__ uint32_t s_m32[4];
@@ -590,8 +588,8 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   const uint64_t* src = a.surv + (size_t)req * a.cap;
   for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
   __syncthreads();
-  block_select_topk<T>(s_keys, (int)n, k, s_sel, s_hist, s_m64, s_m32);
-  commit<T>(a, req, s_sel, k);
+  block_select_topk<T>(s_keys, (int)n, k, s_sel, s_out, s_hist, s_m64, s_m32);
+  commit<T>(a, req, s_out, k);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -659,6 +657,13 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
     if (tid < 32) warp_find_digit_desc(s_hist, krem, &s_m32[0], &s_m32[1]);
     __syncthreads();
     uint32_t d = s_m32[0], above = s_m32[1];
+    if (d >= 256) {   // fewer candidates than BW (flagged request): take them all
+      krem = 0;
+      prefix = 0;
+      mask = 0;
+      __syncthreads();
+      break;
+    }
     uint32_t inbin = s_hist[d];
     krem -= above;
     prefix |= (uint64_t)d << shift;
@@ -683,9 +688,10 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
     });
   }
   __syncthreads();
+  const int kk = min(k, (int)s_m32[2]);
   int P = 1;
-  while (P < k) P <<= 1;
-  for (int i = k + tid; i < P; i += T) s_sel[i] = 0ull;
+  while (P < kk) P <<= 1;
+  for (int i = kk + tid; i < P; i += T) s_sel[i] = 0ull;
   __syncthreads();
   for (int size = 2; size <= P; size <<= 1) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
@@ -702,30 +708,36 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
       __syncthreads();
     }
   }
-  commit<T>(a, req, s_sel, k);
+  commit<T>(a, req, s_sel, kk);
 }
 
 // ---------------------------------------------------------------------------------------------
 // k_sparse: one CTA per request; every legal candidate is formed on chip (no pruning needed).
-// GROUP = 32: one warp per live row; GROUP = T: the whole block on one row (the root step).
+// ROOT: the single root row, gathered by the whole block. Otherwise one THREAD per live row for
+// rows with <= 16 children (all rows' dependent load chains node -> first_child -> labels ->
+// logits run concurrently), and one warp per row for the rare larger rows.
 // ---------------------------------------------------------------------------------------------
-template <int T, int GROUP>
+template <int T, bool ROOT>
 __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_keys[];  // [rows * max_children]
-  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ uint32_t s_hist[256];
   __shared__ uint64_t s_m64[2 * (T / 32)];
   __shared__ uint32_t s_m32[4];
   __shared__ float s_red[T / 32], s_red2[T / 32];
-  __shared__ uint32_t s_count;
+  __shared__ uint32_t s_count, s_nbig;
+  __shared__ int32_t s_big[kMaxBW];
   const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
   const int nl = nlive_of(a, req);
   const LevelDev& L = a.trie.lv[a.level];
   const uint16_t* lab = a.trie.lv[a.level + 1].label;
   const int V = a.trie.V;
-  if (tid == 0) s_count = 0;
+  if (tid == 0) {
+    s_count = 0;
+    s_nbig = 0;
+  }
   __syncthreads();
-  if (GROUP == T) {
+  if (ROOT) {
     for (int b = 0; b < nl; ++b) {
       float S;
       uint32_t node;
@@ -752,8 +764,43 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
       __syncthreads();
     }
   } else {
-    const int warp = tid >> 5;
-    for (int b = warp; b < nl; b += T / 32) {
+    constexpr int kSmall = 16;
+    for (int b = tid; b < nl; b += T) {
+      float S;
+      uint32_t node;
+      row_state(a, req, b, S, node);
+      const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      const int cnt = (int)(fe - fc);
+      if (cnt > kSmall) {
+        s_big[atomicAdd(&s_nbig, 1u)] = b;
+        continue;
+      }
+      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      uint32_t vv[kSmall];
+      float xv[kSmall];
+#pragma unroll
+      for (int k = 0; k < kSmall; ++k) vv[k] = k < cnt ? lab[fc + k] : 0u;
+#pragma unroll
+      for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? row[vv[k]] : -INFINITY;
+      float M = -INFINITY;
+#pragma unroll
+      for (int k = 0; k < kSmall; ++k) M = fmaxf(M, xv[k]);
+      float Z = 0.f;
+#pragma unroll
+      for (int k = 0; k < kSmall; ++k)
+        if (k < cnt) Z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
+      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+      const uint32_t base = atomicAdd(&s_count, (uint32_t)cnt);
+#pragma unroll
+      for (int k = 0; k < kSmall; ++k)
+        if (k < cnt) s_keys[base + k] = make_key(cand_score(S, xv[k], lse), (uint32_t)b * V + vv[k]);
+    }
+    __syncthreads();
+    const int nbig = (int)s_nbig;
+    for (int i = tid >> 5; i < nbig; i += T / 32) {
+      const int b = s_big[i];
       float S;
       uint32_t node;
       row_state(a, req, b, S, node);
@@ -782,8 +829,8 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
   const int n = (int)s_count;
   if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
   const int k = min(n, a.BW);
-  block_select_topk<T>(s_keys, n, k, s_sel, s_hist, s_m64, s_m32);
-  commit<T>(a, req, s_sel, k);
+  block_select_topk<T>(s_keys, n, k, s_sel, s_out, s_hist, s_m64, s_m32);
+  commit<T>(a, req, s_out, k);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -931,29 +978,39 @@ static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s, cud
 }
 
 // Called once per context: opt the variable-shared-memory kernels into their maximum.
+cudaError_t configure_stream_kernels();
+
 cudaError_t configure_kernels(int cap) {
-  cudaError_t e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = configure_stream_kernels();
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)(cap * sizeof(uint64_t)));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_sparse<512, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_sparse<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(kSparseCap * sizeof(uint64_t)));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_sparse<512, 32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(k_sparse<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(kSparseCap * sizeof(uint64_t)));
 }
+
+bool stream_supported(int V);
+cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0,
+                          cudaEvent_t ev1, int* launches);
 
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
   if (sparse_route) {
     size_t smem = (size_t)sparse_keys * sizeof(uint64_t);
-    if (rows == 1) k_sparse<512, 512><<<a.batch, 512, smem, s>>>(a);
-    else k_sparse<512, 32><<<a.batch, 512, smem, s>>>(a);
+    if (rows == 1) k_sparse<512, true><<<a.batch, 512, smem, s>>>(a);
+    else k_sparse<512, false><<<a.batch, 512, smem, s>>>(a);
     ++*launches;
     return cudaGetLastError();
   }
   const int V = a.trie.V;
-  if (V <= 2048) e = launch_dense<128, 4>(a, rows, s, ev0, ev1, launches);
+  if (stream_supported(V)) {
+    e = launch_stream(a, rows, s, ev0, ev1, launches);
+  } else if (V <= 2048) e = launch_dense<128, 4>(a, rows, s, ev0, ev1, launches);
   else if (V <= 4096) e = launch_dense<256, 4>(a, rows, s, ev0, ev1, launches);
   else if (V <= 8192) e = launch_dense<256, 8>(a, rows, s, ev0, ev1, launches);
   else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s, ev0, ev1, launches);

@@ -1,0 +1,673 @@
+// Dense-step kernels for sm_100a: the threshold seed and the
+// persistent streaming pass.
+//
+// k_seed (one CTA per request): rows 0..R0-1 of the request -- the best-scored beams, since slot
+//   scores are sorted ("the log_prob results for each beam are inherently in
+//   descending order") -- are bulk-copied (TMA, cp.async.bulk + mbarrier) into shared memory with
+//   their V-bit legal-children masks (L361, L371). Each row's legal-only log-softmax gives its
+//   candidate scores c = S_b + (x - lse_b) (L376); a count-verified bisection over the UNION of
+//   those candidates finds theta with at least BW candidates >= theta, so theta <= the request's
+//   true BW-th best score (the heap minimum of L385 can only be higher). The seed rows' own
+//   candidates >= theta are emitted to the survivor buffer.
+// k_stream (persistent, warp-specialised): the remaining live rows in b-major order. A producer
+//   warp fetches 32 rows' metadata at once, drops rows with S_b < theta before reading them
+//   (early termination, L385: every candidate of the row is <= S_b), and issues two bulk copies
+//   per remaining dense row into a ring of NS shared-memory stages. CT consumer threads (thread
+//   t owns the 32 tokens of mask word t) load the stage into registers (rotated, conflict-free
+//   LDS.128), release it, compute m, Z, lse with f32x2 arithmetic and fixed-order reductions,
+//   skip the row if UB_b = S_b - ln Z_b < theta, and emit c >= theta with warp-aggregated
+//   atomics. Pruning is strict (c < theta dropped), so results never depend on theta
+//   (R16).
+// Sparse-parent rows inside a dense step are gathered by label from global memory.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "xgr_internal.cuh"
+
+namespace xgr {
+
+namespace {
+
+constexpr float kLog2eS = 1.4426950408889634f;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                         uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float wmax(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float wsum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ void emit(uint64_t key, uint32_t* count, uint64_t* buf, int cap) {
+  unsigned m = __activemask();
+  int leader = __ffs(m) - 1;
+  int lane = threadIdx.x & 31;
+  uint32_t base = 0;
+  if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
+  base = __shfl_sync(m, base, leader);
+  uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
+  if (pos < (uint32_t)cap) buf[pos] = key;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+struct Desc {
+  int32_t req, b, kind, slot;  // kind: 0 nothing to do, 1 dense row in stage, 2 sparse row
+  float S;
+  uint32_t node;
+};
+
+// Consumer-group reductions: warp butterfly, then every consumer thread folds the per-warp
+// partials in a fixed order (bitwise-identical, deterministic results in every thread).
+template <int CT>
+__device__ __forceinline__ float cmax(float v, float* part) {
+  v = wmax(v);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  named_sync(1, CT);
+  float r = part[0];
+#pragma unroll
+  for (int i = 1; i < CT / 32; ++i) r = fmaxf(r, part[i]);
+  return r;
+}
+template <int CT>
+__device__ __forceinline__ float csum(float v, float* part) {
+  v = wsum(v);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  named_sync(1, CT);
+  float r = part[0];
+#pragma unroll
+  for (int i = 1; i < CT / 32; ++i) r += part[i];
+  return r;
+}
+template <int CT>
+__device__ __forceinline__ int cisum(int v, int* part) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  named_sync(1, CT);
+  int r = 0;
+#pragma unroll
+  for (int i = 0; i < CT / 32; ++i) r += part[i];
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------------------------------
+// k_seed
+// ------------------------------------------------------------------------------------------
+template <int CTR, int R0>
+__global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ StepArgs a) {
+  constexpr int NT = CTR * R0;
+  extern __shared__ __align__(128) float s_dyn[];
+  float* s_row = s_dyn;                                                   // [R0][32*CTR]
+  uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dyn + R0 * 32 * CTR);  // [R0][CTR]
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int r_kind[R0], r_slot[R0];
+  __shared__ float r_S[R0];
+  __shared__ float g_max[NT / 32], g_sum[NT / 32];
+  __shared__ float b_red[2][NT / 32];
+  __shared__ int b_cnt[2][NT / 32];
+  const int tid = threadIdx.x, req = blockIdx.x;
+  const int g = tid / CTR, lt = tid - g * CTR, lane = tid & 31;
+  const int V = a.trie.V, W = a.trie.W, BW = a.BW;
+  const LevelDev& L = a.trie.lv[a.level];
+  const int nl = nlive_of(a, req);
+
+  if (tid < R0) {
+    int kind = 0, slot = -1;
+    float S = 0.f;
+    if (tid < nl) {
+      uint32_t node;
+      row_state(a, req, tid, S, node);
+      slot = L.dense_slot ? L.dense_slot[node] : -1;
+      kind = slot >= 0 ? 1 : 0;   // sparse seed rows are left to k_stream
+    }
+    r_kind[tid] = kind;
+    r_slot[tid] = slot;
+    r_S[tid] = S;
+  }
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < R0 * CTR; i += NT) s_msk[i] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t bytes = 0;
+    for (int r = 0; r < R0; ++r) bytes += r_kind[r] ? (uint32_t)(V + W) * 4u : 0u;
+    if (bytes) {
+      mbar_arrive_tx(&bar, bytes);
+      const uint64_t pol = policy_evict_first();
+      for (int r = 0; r < R0; ++r) {
+        if (!r_kind[r]) continue;
+        const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
+        bulk_g2s(s_row + (size_t)r * 32 * CTR, row, (uint32_t)V * 4u, &bar, pol);
+        bulk_g2s(s_msk + (size_t)r * CTR, L.bitmap + (size_t)r_slot[r] * W, (uint32_t)W * 4u, &bar, pol);
+      }
+    } else {
+      mbar_arrive(&bar);
+    }
+  }
+  mbar_wait(&bar, 0);
+
+  int kind = r_kind[g];
+  const float S = r_S[g];
+  float c[32];
+  uint32_t wraw = 0, wm = 0;
+  float cmaxv = -INFINITY;
+  int nleg = 0;
+  if (kind) {
+    const float* srow = s_row + (size_t)g * 32 * CTR;
+    wraw = s_msk[g * CTR + lt];
+    wm = __funnelshift_r(wraw, wraw, 4 * (lt & 7));
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 x = *reinterpret_cast<const float4*>(srow + 32 * lt + 4 * ((i + lt) & 7));
+      c[4 * i + 0] = (wm >> (4 * i + 0)) & 1u ? x.x : -INFINITY;
+      c[4 * i + 1] = (wm >> (4 * i + 1)) & 1u ? x.y : -INFINITY;
+      c[4 * i + 2] = (wm >> (4 * i + 2)) & 1u ? x.z : -INFINITY;
+      c[4 * i + 3] = (wm >> (4 * i + 3)) & 1u ? x.w : -INFINITY;
+      tmax = fmaxf(tmax, fmaxf(fmaxf(c[4 * i], c[4 * i + 1]), fmaxf(c[4 * i + 2], c[4 * i + 3])));
+    }
+    // group (= row) reductions on named barrier 1 + g
+    float v = wmax(tmax);
+    if (lane == 0) g_max[tid >> 5] = v;
+    named_sync(1 + g, CTR);
+    float M = g_max[g * (CTR / 32)];
+#pragma unroll
+    for (int i = 1; i < CTR / 32; ++i) M = fmaxf(M, g_max[g * (CTR / 32) + i]);
+    const float2 nM = make_float2(-M, -M), l2e = make_float2(kLog2eS, kLog2eS);
+    float2 z0 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      float2 t = __fmul2_rn(__fadd2_rn(make_float2(c[2 * i], c[2 * i + 1]), nM), l2e);
+      z0 = __fadd2_rn(z0, make_float2(ex2f(t.x), ex2f(t.y)));
+    }
+    v = wsum(z0.x + z0.y);
+    if (lane == 0) g_sum[tid >> 5] = v;
+    named_sync(1 + g, CTR);
+    float Z = g_sum[g * (CTR / 32)];
+#pragma unroll
+    for (int i = 1; i < CTR / 32; ++i) Z += g_sum[g * (CTR / 32) + i];
+    const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+    const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    if (lt == 0) {
+      a.lse[(size_t)req * BW + g] = finite ? lse : __int_as_float(0x7fc00000);
+      if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+      if (a.counters_on) {
+        atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
+      }
+    }
+    if (finite) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        c[i] = cand_score(S, c[i], lse);   // -inf stays -inf
+        cmaxv = fmaxf(cmaxv, c[i]);
+      }
+      nleg = __popc(wraw);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) c[i] = -INFINITY;
+      kind = 0;   // a flagged row emits nothing
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) c[i] = -INFINITY;
+  }
+  if (a.counters_on) {
+    int lc = __reduce_add_sync(0xffffffffu, r_kind[g] ? __popc(wraw) : 0);
+    if (lane == 0 && lc) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
+  }
+
+  // block-wide (union of the seed rows) threshold: histogram of hi0 - c over [0, 16) in 1024
+  // bins of 1/64, cumulative count from the top, then an exact count verifies the bound.
+  auto bmax = [&](float x) {
+    x = wmax(x);
+    if (lane == 0) b_red[0][tid >> 5] = x;
+    __syncthreads();
+    float r = b_red[0][0];
+#pragma unroll
+    for (int i = 1; i < NT / 32; ++i) r = fmaxf(r, b_red[0][i]);
+    return r;
+  };
+  auto bcnt = [&](int x, int buf) {
+    x = __reduce_add_sync(0xffffffffu, x);
+    if (lane == 0) b_cnt[buf][tid >> 5] = x;
+    __syncthreads();
+    int r = 0;
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) r += b_cnt[buf][i];
+    return r;
+  };
+  const float hi0 = bmax(cmaxv);
+  const int total = bcnt(nleg, 0);
+  float lo = -INFINITY;
+  if (!a.no_prune && total >= BW && hi0 > -INFINITY) {
+    constexpr int NB = NT;            // one bin per thread
+    constexpr float kRange = 16.0f;
+    constexpr float kScale = NB / kRange;
+    uint32_t* hist = reinterpret_cast<uint32_t*>(s_row);   // the rows are in registers now
+    __syncthreads();
+    hist[tid] = 0u;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float dd = (hi0 - c[i]) * kScale;
+      if (dd < (float)NB) atomicAdd(&hist[(int)dd], 1u);   // -inf / NaN never pass
+    }
+    __syncthreads();
+    // inclusive scan of the bins (bin t = thread t): warp scan, then warp offsets
+    uint32_t v = hist[tid];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += y;
+    }
+    if (lane == 31) b_cnt[1][tid >> 5] = (int)v;
+    __syncthreads();
+    uint32_t off = 0;
+    for (int i = 0; i < (tid >> 5); ++i) off += (uint32_t)b_cnt[1][i];
+    v += off;
+    const uint32_t prev = v - hist[tid];
+    if (tid == 0) b_red[1][0] = -1.0f;
+    __syncthreads();
+    if (v >= (uint32_t)BW && prev < (uint32_t)BW) b_red[1][0] = (float)tid;
+    __syncthreads();
+    const float tb = b_red[1][0];
+    if (tb >= 0.0f) {
+      // every value counted in bins <= tb has c > hi0 - (tb + 1) / kScale; half a bin of margin
+      const float cand = hi0 - (tb + 1.5f) / kScale;
+      int n = 0;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) n += c[i] >= cand;
+      if (bcnt(n, 0) >= BW) lo = cand;
+    }
+  }
+  if (tid == 0) a.theta[req] = lo > -INFINITY ? f2o(lo) : 0u;
+  // emit the seed rows' candidates >= theta (lo == -inf: every legal candidate)
+  int ns = 0;
+  if (kind && cmaxv >= lo) {
+    const uint32_t fbase = (uint32_t)g * (uint32_t)V;
+    uint32_t* cnt = a.surv_count + req;
+    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      if (((wm >> i) & 1u) && c[i] >= lo) {
+        const uint32_t v = 32u * lt + 4u * (((i >> 2) + lt) & 7) + (i & 3);
+        emit(make_key(c[i], fbase + v), cnt, sbuf, a.cap);
+        ++ns;
+      }
+    }
+  }
+  if (a.counters_on) {
+    const int tot = __reduce_add_sync(0xffffffffu, ns);
+    if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// k_stream: G consumer groups of 256 threads (thread t of a group owns EPT consecutive tokens,
+// EPT/32 mask words) process different rows concurrently; one producer warp feeds them.
+// ------------------------------------------------------------------------------------------
+template <int EPT>
+__device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
+  if constexpr (EPT == 32) {
+    const uint32_t w = msk[lt];
+    return (uint64_t)__funnelshift_r(w, w, 4 * (lt & 7));
+  } else {
+    const uint64_t m = (uint64_t)msk[2 * lt] | ((uint64_t)msk[2 * lt + 1] << 32);
+    const int r = 4 * (lt & 15);
+    return r ? (m >> r) | (m << (64 - r)) : m;
+  }
+}
+
+template <int EPT, int G, int NS>
+__global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constant__ StepArgs a, int total,
+                                                             int seeded_rows) {
+  constexpr int GT = 256;          // consumer threads per group
+  constexpr int VT = GT * EPT;     // tokens per stage row
+  constexpr int MW = VT / 32;      // mask words per stage
+  constexpr int NF4 = EPT / 4;     // float4 per thread
+  constexpr int NC = GT * G;       // consumer threads
+  extern __shared__ __align__(128) float s_dyn[];
+  float* s_row = s_dyn;                                             // [NS][VT]
+  uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dyn + NS * VT);  // [NS][MW]
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  __shared__ Desc desc[NS];
+  __shared__ float s_th[NS];
+  __shared__ float p_max[G][GT / 32], p_sum[G][GT / 32];
+  __shared__ int p_leg[G][GT / 32];
+
+  const int tid = threadIdx.x;
+  const int V = a.trie.V;
+  const int W = a.trie.W;
+  const LevelDev& L = a.trie.lv[a.level];
+  const int BW = a.BW;
+
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = tid; i < NS * MW; i += NC + 32) s_msk[i] = 0u;
+  __syncthreads();
+
+  if (tid >= NC) {
+    // ------------------------------- producer warp ---------------------------------------
+    const int lane = tid & 31;
+    const uint64_t pol = policy_evict_first();
+    for (int k0 = 0;; k0 += 32) {
+      if (blockIdx.x + k0 * gridDim.x >= total) break;
+      // every lane fetches one upcoming row's metadata (independent loads in parallel)
+      const int k = k0 + lane;
+      const int w = blockIdx.x + k * gridDim.x;
+      int kind = 0, slot = -1, b = 0, req = 0;
+      float S = 0.f, th = -INFINITY;
+      uint32_t node = 0;
+      if (w < total) {
+        b = w / a.batch;
+        req = w - b * a.batch;
+        const int nl = a.nlive_in ? a.nlive_in[req] : 1;
+        if (b < nl) {
+          row_state(a, req, b, S, node);
+          th = theta_value(a.theta[req]);
+          slot = L.dense_slot ? L.dense_slot[node] : -1;
+          if (S < th) {
+            a.lse[(size_t)req * BW + b] = __int_as_float(0x7fc00000);
+            if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
+          } else if (slot >= 0 && b < seeded_rows) {
+            kind = 0;   // done by k_seed
+          } else {
+            kind = slot >= 0 ? 1 : 2;
+          }
+        }
+      }
+      for (int j = 0; j < 32; ++j) {
+        const int kj = k0 + j;
+        if (blockIdx.x + kj * gridDim.x >= total) break;
+        const int jkind = __shfl_sync(0xffffffffu, kind, j);
+        const int jslot = __shfl_sync(0xffffffffu, slot, j);
+        const int jb = __shfl_sync(0xffffffffu, b, j);
+        const int jreq = __shfl_sync(0xffffffffu, req, j);
+        const float jS = __shfl_sync(0xffffffffu, S, j);
+        const float jth = __shfl_sync(0xffffffffu, th, j);
+        const uint32_t jnode = __shfl_sync(0xffffffffu, node, j);
+        if (lane == 0) {
+          const int st = kj % NS;
+          if (kj >= NS) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
+          Desc d;
+          d.req = jreq;
+          d.b = jb;
+          d.kind = jkind;
+          d.slot = jslot;
+          d.S = jS;
+          d.node = jnode;
+          desc[st] = d;
+          s_th[st] = jth;
+          if (jkind == 1) {
+            const float* row = a.logits + (size_t)jreq * a.req_stride + (size_t)jb * a.ld;
+            const uint32_t rb = (uint32_t)V * 4u, mb = (uint32_t)W * 4u;
+            mbar_arrive_tx(&full[st], rb + mb);
+            bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
+            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W, mb, &full[st], pol);
+          } else {
+            mbar_arrive(&full[st]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+
+  // ------------------------------- consumer groups ----------------------------------------
+  const int g = tid / GT, lt = tid - g * GT, lane = tid & 31;
+  const int bar_id = 1 + g;
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  float* pmax = p_max[g];
+  float* psum = p_sum[g];
+  auto gmax = [&](float v) {
+    v = wmax(v);
+    if (lane == 0) pmax[lt >> 5] = v;
+    named_sync(bar_id, GT);
+    float r = pmax[0];
+#pragma unroll
+    for (int i = 1; i < GT / 32; ++i) r = fmaxf(r, pmax[i]);
+    return r;
+  };
+  auto gsum = [&](float v) {
+    v = wsum(v);
+    if (lane == 0) psum[lt >> 5] = v;
+    named_sync(bar_id, GT);
+    float r = psum[0];
+#pragma unroll
+    for (int i = 1; i < GT / 32; ++i) r += psum[i];
+    return r;
+  };
+  for (int k = g;; k += G) {
+    const int w = blockIdx.x + k * gridDim.x;
+    if (w >= total) break;
+    const int st = k % NS;
+    mbar_wait(&full[st], (k / NS) & 1);
+    const Desc d = desc[st];
+    const float th = s_th[st];
+    const int req = d.req, b = d.b;
+    const float S = d.S;
+    const uint32_t fbase = (uint32_t)b * (uint32_t)V;
+    uint32_t* cnt = a.surv_count + req;
+    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+
+    if (d.kind != 1) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (d.kind == 0) continue;
+      // sparse parent inside a dense step: gather the legal logits by label (rare)
+      if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
+      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const uint32_t fc = L.first_child[d.node], fe = L.first_child[d.node + 1];
+      float tm = -INFINITY;
+      for (uint32_t q = fc + lt; q < fe; q += GT) tm = fmaxf(tm, row[lab[q]]);
+      const float M = gmax(tm);
+      float z = 0.f;
+      for (uint32_t q = fc + lt; q < fe; q += GT)
+        z += ex2f(__fmul_rn(__fsub_rn(row[lab[q]], M), kLog2eS));
+      const float Z = gsum(z);
+      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      if (lt == 0) {
+        a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
+        if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+        if (a.counters_on) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)(fe - fc));
+      }
+      if (!finite) continue;
+      if (!(cand_score(S, M, lse) >= th)) continue;
+      for (uint32_t q = fc + lt; q < fe; q += GT) {
+        const uint32_t v = lab[q];
+        const float c = cand_score(S, row[v], lse);
+        if (c >= th) emit(make_key(c, fbase + v), cnt, sbuf, a.cap);
+      }
+      continue;
+    }
+
+    // ---- dense row: stage -> registers (thread lt owns tokens [EPT*lt, EPT*lt + EPT)) ----
+    const float* srow = s_row + (size_t)st * VT + EPT * lt;
+    const uint64_t wm = stage_mask<EPT>(s_msk + (size_t)st * MW, lt);
+    float4 x[NF4];
+#pragma unroll
+    for (int i = 0; i < NF4; ++i)
+      x[i] = *reinterpret_cast<const float4*>(srow + 4 * ((i + lt) & (NF4 - 1)));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < NF4; ++i) {
+      x[i].x = (wm >> (4 * i + 0)) & 1ull ? x[i].x : -INFINITY;
+      x[i].y = (wm >> (4 * i + 1)) & 1ull ? x[i].y : -INFINITY;
+      x[i].z = (wm >> (4 * i + 2)) & 1ull ? x[i].z : -INFINITY;
+      x[i].w = (wm >> (4 * i + 3)) & 1ull ? x[i].w : -INFINITY;
+      tmax = fmaxf(tmax, fmaxf(fmaxf(x[i].x, x[i].y), fmaxf(x[i].z, x[i].w)));
+    }
+    const float M = gmax(tmax);
+    const float2 nM = make_float2(-M, -M);
+    const float2 l2e = make_float2(kLog2eS, kLog2eS);
+    float2 z0 = make_float2(0.f, 0.f), z1 = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NF4; ++i) {
+      float2 a0 = __fmul2_rn(__fadd2_rn(make_float2(x[i].x, x[i].y), nM), l2e);
+      float2 a1 = __fmul2_rn(__fadd2_rn(make_float2(x[i].z, x[i].w), nM), l2e);
+      z0 = __fadd2_rn(z0, make_float2(ex2f(a0.x), ex2f(a0.y)));
+      z1 = __fadd2_rn(z1, make_float2(ex2f(a1.x), ex2f(a1.y)));
+    }
+    const float2 zz = __fadd2_rn(z0, z1);
+    const float Z = gsum(zz.x + zz.y);
+    const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+    const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    if (lt == 0) {
+      a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
+      if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+      if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
+    }
+    if (a.counters_on) {
+      int lc = __reduce_add_sync(0xffffffffu, (int)__popcll(wm));
+      if (lane == 0) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
+    }
+    if (!finite) continue;
+    if (!(cand_score(S, M, lse) >= th)) {  // UB_b = S_b - ln Z_b < theta: nothing to emit
+      if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
+      continue;
+    }
+    // conservative pre-filter on x (the exact test c >= theta follows)
+    const float xthr = (th == -INFINITY)
+                           ? -INFINITY
+                           : (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
+    int ns = 0;
+    if (tmax >= xthr) {
+#pragma unroll
+      for (int i = 0; i < NF4; ++i) {
+        const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
+        if (fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])) >= xthr) {
+          const uint32_t v0 = (uint32_t)(EPT * lt + 4 * ((i + lt) & (NF4 - 1)));
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            if (((wm >> (4 * i + j)) & 1ull) && xs[j] >= xthr) {
+              const float c = cand_score(S, xs[j], lse);
+              if (c >= th) {
+                emit(make_key(c, fbase + v0 + j), cnt, sbuf, a.cap);
+                ++ns;
+              }
+            }
+          }
+        }
+      }
+    }
+    if (a.counters_on) {
+      const int tot = __reduce_add_sync(0xffffffffu, ns);
+      if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
+    }
+  }
+}
+
+template <int EPT, int NS>
+static size_t stream_smem() {
+  return (size_t)NS * (256 * EPT * sizeof(float) + 256 * EPT / 8);
+}
+
+static int g_num_sms = 0;
+
+cudaError_t configure_stream_kernels() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_stream<32, 3, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)stream_smem<32, 6>());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_stream<64, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)stream_smem<64, 3>());
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_seed<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)stream_smem<32, 4>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_seed<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)stream_smem<64, 2>());
+}
+
+// Usable when a row and its mask can be bulk-copied: V % 128 == 0 (16-byte mask rows), V <= 16384.
+bool stream_supported(int V) { return V % 128 == 0 && V <= 16384; }
+
+// Dense step: seed (theta + rows 0..R0-1), then the streaming pass over the rest. Returns the
+// number of kernels launched through *launches; ev0/ev1 bracket the streaming kernel.
+cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0,
+                          cudaEvent_t ev1, int* launches) {
+  const int total = a.batch * rows;
+  const int sms = g_num_sms > 0 ? g_num_sms : 148;
+  const int grid = std::min(total, sms);
+  if (a.trie.V <= 8192) {
+    k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+    if (ev0) cudaEventRecord(ev0, s);
+    k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, 4);
+  } else {
+    k_seed<512, 2><<<a.batch, 1024, stream_smem<64, 2>(), s>>>(a);
+    if (ev0) cudaEventRecord(ev0, s);
+    k_stream<64, 2, 3><<<grid, 2 * 256 + 32, stream_smem<64, 3>(), s>>>(a, total, 2);
+  }
+  if (ev1) cudaEventRecord(ev1, s);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace xgr

@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
   __shared__ Desc desc[NS];
   __shared__ float s_th[NS];
   __shared__ float p_max[G][GT / 32], p_sum[G][GT / 32];
-  __shared__ int p_leg[G][GT / 32];
+  __shared__ float2 part[G][2][GT / 32];
 
   const int tid = threadIdx.x;
   const int V = a.trie.V;
@@ -496,6 +496,7 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
     for (int i = 1; i < GT / 32; ++i) r += psum[i];
     return r;
   };
+  int it = 0;   // this group's dense-row count: parity selects the partials buffer
   for (int k = g;; k += G) {
     const int w = blockIdx.x + k * gridDim.x;
     if (w >= total) break;
@@ -505,9 +506,6 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
     const float th = s_th[st];
     const int req = d.req, b = d.b;
     const float S = d.S;
-    const uint32_t fbase = (uint32_t)b * (uint32_t)V;
-    uint32_t* cnt = a.surv_count + req;
-    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
 
     if (d.kind != 1) {
       __syncwarp();
@@ -533,46 +531,66 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
       }
       if (!finite) continue;
       if (!(cand_score(S, M, lse) >= th)) continue;
+      const uint32_t fbase = (uint32_t)b * (uint32_t)V;
       for (uint32_t q = fc + lt; q < fe; q += GT) {
         const uint32_t v = lab[q];
         const float c = cand_score(S, row[v], lse);
-        if (c >= th) emit(make_key(c, fbase + v), cnt, sbuf, a.cap);
+        if (c >= th) emit(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap, a.cap);
       }
       continue;
     }
 
-    // ---- dense row: stage -> registers (thread lt owns tokens [EPT*lt, EPT*lt + EPT)) ----
-    const float* srow = s_row + (size_t)st * VT + EPT * lt;
-    const uint64_t wm = stage_mask<EPT>(s_msk + (size_t)st * MW, lt);
-    float4 x[NF4];
+    // ---- dense row: stage -> registers. Thread lt owns float4 q = i*GT + lt (i < NF4): 16-byte
+    // consecutive per lane, conflict-free, compile-time offsets; its mask nibble is bits
+    // 4*(lt & 7) .. +3 of word q / 8 = i*GT/8 + lt/8.
+    const float* srow = s_row + (size_t)st * VT + 4 * lt;
+    const uint32_t* smsk = s_msk + (size_t)st * MW + (lt >> 3);
+    const int nsh = 4 * (lt & 7);
+    float x[EPT];
 #pragma unroll
-    for (int i = 0; i < NF4; ++i)
-      x[i] = *reinterpret_cast<const float4*>(srow + 4 * ((i + lt) & (NF4 - 1)));
+    for (int i = 0; i < NF4; ++i) {
+      const float4 v4 = *reinterpret_cast<const float4*>(srow + i * GT * 4);
+      const uint32_t nb = smsk[i * (GT / 8)] >> nsh;
+      x[4 * i] = (nb & 1u) ? v4.x : -INFINITY;
+      x[4 * i + 1] = (nb & 2u) ? v4.y : -INFINITY;
+      x[4 * i + 2] = (nb & 4u) ? v4.z : -INFINITY;
+      x[4 * i + 3] = (nb & 8u) ? v4.w : -INFINITY;
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
 
     float tmax = -INFINITY;
 #pragma unroll
-    for (int i = 0; i < NF4; ++i) {
-      x[i].x = (wm >> (4 * i + 0)) & 1ull ? x[i].x : -INFINITY;
-      x[i].y = (wm >> (4 * i + 1)) & 1ull ? x[i].y : -INFINITY;
-      x[i].z = (wm >> (4 * i + 2)) & 1ull ? x[i].z : -INFINITY;
-      x[i].w = (wm >> (4 * i + 3)) & 1ull ? x[i].w : -INFINITY;
-      tmax = fmaxf(tmax, fmaxf(fmaxf(x[i].x, x[i].y), fmaxf(x[i].z, x[i].w)));
-    }
-    const float M = gmax(tmax);
-    const float2 nM = make_float2(-M, -M);
+    for (int e = 0; e < EPT; e += 4) tmax = fmaxf(tmax, fmaxf(fmaxf(x[e], x[e + 1]), fmaxf(x[e + 2], x[e + 3])));
+    // warp-local (m_w, z_w), one group barrier, then combine the GT/32 pairs
+    const float mw = wmax(tmax);
+    const float mws = mw == -INFINITY ? 0.0f : mw;
+    const float2 nM = make_float2(-mws, -mws);
     const float2 l2e = make_float2(kLog2eS, kLog2eS);
     float2 z0 = make_float2(0.f, 0.f), z1 = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < NF4; ++i) {
-      float2 a0 = __fmul2_rn(__fadd2_rn(make_float2(x[i].x, x[i].y), nM), l2e);
-      float2 a1 = __fmul2_rn(__fadd2_rn(make_float2(x[i].z, x[i].w), nM), l2e);
+    for (int e = 0; e < EPT; e += 4) {
+      const float2 a0 = __fmul2_rn(__fadd2_rn(make_float2(x[e], x[e + 1]), nM), l2e);
+      const float2 a1 = __fmul2_rn(__fadd2_rn(make_float2(x[e + 2], x[e + 3]), nM), l2e);
       z0 = __fadd2_rn(z0, make_float2(ex2f(a0.x), ex2f(a0.y)));
       z1 = __fadd2_rn(z1, make_float2(ex2f(a1.x), ex2f(a1.y)));
     }
     const float2 zz = __fadd2_rn(z0, z1);
-    const float Z = gsum(zz.x + zz.y);
+    const float zw = wsum(zz.x + zz.y);
+    float2* pp = part[g][it & 1];
+    if (lane == 0) pp[lt >> 5] = make_float2(mw, zw);
+    named_sync(bar_id, GT);
+    ++it;
+    float2 pr = lane < GT / 32 ? pp[lane] : make_float2(-INFINITY, 0.f);
+    float M = pr.x;
+#pragma unroll
+    for (int o = GT / 64; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float zi = pr.y * ex2f(__fmul_rn(__fsub_rn(pr.x, M), kLog2eS));
+    if (lane >= GT / 32) zi = 0.f;
+#pragma unroll
+    for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
+    M = __shfl_sync(0xffffffffu, M, 0);
+    const float Z = __shfl_sync(0xffffffffu, zi, 0);
     const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
     const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
     if (lt == 0) {
@@ -581,7 +599,10 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
       if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
     }
     if (a.counters_on) {
-      int lc = __reduce_add_sync(0xffffffffu, (int)__popcll(wm));
+      int lc = 0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) lc += x[e] > -INFINITY;
+      lc = __reduce_add_sync(0xffffffffu, lc);
       if (lane == 0) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
     }
     if (!finite) continue;
@@ -589,26 +610,40 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
     }
-    // conservative pre-filter on x (the exact test c >= theta follows)
-    const float xthr = (th == -INFINITY)
-                           ? -INFINITY
-                           : (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
     int ns = 0;
-    if (tmax >= xthr) {
+    const uint32_t fbase = (uint32_t)b * (uint32_t)V;
+    uint32_t* cnt = a.surv_count + req;
+    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+    if (th > -INFINITY) {
+      // conservative pre-filter on x (the exact test c >= theta follows); illegal x are -inf
+      const float xthr = (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
+      if (tmax >= xthr) {
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if (x[e] >= xthr) {
+            const float c = cand_score(S, x[e], lse);
+            if (c >= th) {
+              const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
+              emit(make_key(c, fbase + v), cnt, sbuf, a.cap);
+              ++ns;
+            }
+          }
+        }
+      }
+    } else {
+      // no bound (pruning off or too few seed candidates): every legal token, -inf logits
+      // included, is a candidate; legality re-read from the node's bitmap in global memory
+      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (lt >> 3);
 #pragma unroll
       for (int i = 0; i < NF4; ++i) {
-        const float xs[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
-        if (fmaxf(fmaxf(xs[0], xs[1]), fmaxf(xs[2], xs[3])) >= xthr) {
-          const uint32_t v0 = (uint32_t)(EPT * lt + 4 * ((i + lt) & (NF4 - 1)));
+        const uint32_t q4 = (uint32_t)(i * GT + lt);
+        const uint32_t nb = (4 * q4 < (uint32_t)V) ? (__ldg(gm + i * (GT / 8)) >> nsh) : 0u;
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            if (((wm >> (4 * i + j)) & 1ull) && xs[j] >= xthr) {
-              const float c = cand_score(S, xs[j], lse);
-              if (c >= th) {
-                emit(make_key(c, fbase + v0 + j), cnt, sbuf, a.cap);
-                ++ns;
-              }
-            }
+        for (int j = 0; j < 4; ++j) {
+          if ((nb >> j) & 1u) {
+            const float c = cand_score(S, x[4 * i + j], lse);
+            emit(make_key(c, fbase + 4u * q4 + j), cnt, sbuf, a.cap);
+            ++ns;
           }
         }
       }

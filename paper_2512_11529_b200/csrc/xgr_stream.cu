@@ -22,6 +22,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "xgr_internal.cuh"
 
@@ -371,8 +372,8 @@ __device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
   }
 }
 
-template <int EPT, int G, int NS>
-__global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constant__ StepArgs a, int total,
+template <int EPT, int G, int NS, int MINB = 1>
+__global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   constexpr int GT = 256;          // consumer threads per group
   constexpr int VT = GT * EPT;     // tokens per stage row
@@ -406,44 +407,69 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
 
   if (tid >= NC) {
     // ------------------------------- producer warp ---------------------------------------
+    // Lane j holds the metadata of row k0 + j of the current batch of 32. Three batches are in
+    // flight: raw loads (nlive, S, node, theta) for batch n+2, the dependent dense_slot load for
+    // batch n+1, and the copies of batch n, so no round trip is exposed between batches.
     const int lane = tid & 31;
     const uint64_t pol = policy_evict_first();
+    struct Meta {
+      int b, req, live;
+      float S, th;
+      uint32_t node;
+      int slot;
+    };
+    auto fetch_raw = [&](int k0) {
+      Meta m;
+      const int w = blockIdx.x + (k0 + lane) * gridDim.x;
+      m.b = 0;
+      m.req = 0;
+      m.live = 0;
+      m.S = 0.f;
+      m.th = -INFINITY;
+      m.node = 0;
+      m.slot = -1;
+      if (w < total) {
+        m.b = w / a.batch;
+        m.req = w - m.b * a.batch;
+        const int nl = a.nlive_in ? a.nlive_in[m.req] : 1;
+        m.live = m.b < nl;
+        if (m.live) {
+          row_state(a, m.req, m.b, m.S, m.node);
+          m.th = theta_value(a.theta[m.req]);
+        }
+      }
+      return m;
+    };
+    auto fetch_slot = [&](Meta& m) {
+      if (m.live) m.slot = L.dense_slot ? L.dense_slot[m.node] : -1;
+    };
+    Meta m0 = fetch_raw(0);
+    fetch_slot(m0);
+    Meta m1 = fetch_raw(32);
     for (int k0 = 0;; k0 += 32) {
       if (blockIdx.x + k0 * gridDim.x >= total) break;
-      // every lane fetches one upcoming row's metadata (independent loads in parallel)
-      const int k = k0 + lane;
-      const int w = blockIdx.x + k * gridDim.x;
-      int kind = 0, slot = -1, b = 0, req = 0;
-      float S = 0.f, th = -INFINITY;
-      uint32_t node = 0;
-      if (w < total) {
-        b = w / a.batch;
-        req = w - b * a.batch;
-        const int nl = a.nlive_in ? a.nlive_in[req] : 1;
-        if (b < nl) {
-          row_state(a, req, b, S, node);
-          th = theta_value(a.theta[req]);
-          slot = L.dense_slot ? L.dense_slot[node] : -1;
-          if (S < th) {
-            a.lse[(size_t)req * BW + b] = __int_as_float(0x7fc00000);
-            if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
-          } else if (slot >= 0 && b < seeded_rows) {
-            kind = 0;   // done by k_seed
-          } else {
-            kind = slot >= 0 ? 1 : 2;
-          }
+      Meta m2 = fetch_raw(k0 + 64);
+      fetch_slot(m1);
+      // decisions for the current batch (its loads completed during the previous batch)
+      int kind = 0;
+      if (m0.live) {
+        if (m0.S < m0.th) {   // every candidate of the row is <= S_b < theta: skip unread
+          a.lse[(size_t)m0.req * BW + m0.b] = __int_as_float(0x7fc00000);
+          if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
+        } else if (!(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
+          kind = m0.slot >= 0 ? 1 : 2;
         }
       }
       for (int j = 0; j < 32; ++j) {
         const int kj = k0 + j;
         if (blockIdx.x + kj * gridDim.x >= total) break;
         const int jkind = __shfl_sync(0xffffffffu, kind, j);
-        const int jslot = __shfl_sync(0xffffffffu, slot, j);
-        const int jb = __shfl_sync(0xffffffffu, b, j);
-        const int jreq = __shfl_sync(0xffffffffu, req, j);
-        const float jS = __shfl_sync(0xffffffffu, S, j);
-        const float jth = __shfl_sync(0xffffffffu, th, j);
-        const uint32_t jnode = __shfl_sync(0xffffffffu, node, j);
+        const int jslot = __shfl_sync(0xffffffffu, m0.slot, j);
+        const int jb = __shfl_sync(0xffffffffu, m0.b, j);
+        const int jreq = __shfl_sync(0xffffffffu, m0.req, j);
+        const float jS = __shfl_sync(0xffffffffu, m0.S, j);
+        const float jth = __shfl_sync(0xffffffffu, m0.th, j);
+        const uint32_t jnode = __shfl_sync(0xffffffffu, m0.node, j);
         if (lane == 0) {
           const int st = kj % NS;
           if (kj >= NS) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
@@ -468,6 +494,8 @@ __global__ void __launch_bounds__(256 * G + 32, 1) k_stream(const __grid_constan
         }
         __syncwarp();
       }
+      m0 = m1;
+      m1 = m2;
     }
     return;
   }
@@ -661,6 +689,12 @@ static size_t stream_smem() {
 }
 
 static int g_num_sms = 0;
+static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
+
+template <typename K>
+static cudaError_t opt_in(K k, size_t smem) {
+  return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
 
 cudaError_t configure_stream_kernels() {
   int dev = 0;
@@ -668,17 +702,13 @@ cudaError_t configure_stream_kernels() {
   if (e != cudaSuccess) return e;
   e = cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_stream<32, 3, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stream_smem<32, 6>());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_stream<64, 2, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stream_smem<64, 3>());
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_seed<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)stream_smem<32, 4>());
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_seed<512, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)stream_smem<64, 2>());
+  if (const char* v = getenv("XGR_STREAM_VARIANT")) g_stream_variant = atoi(v);
+  if ((e = opt_in(k_stream<32, 3, 6>, stream_smem<32, 6>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 2, 3>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 1, 4>, stream_smem<32, 1>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<64, 2, 3>, stream_smem<64, 3>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_seed<256, 4>, stream_smem<32, 4>())) != cudaSuccess) return e;
+  return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
 // Usable when a row and its mask can be bulk-copied: V % 128 == 0 (16-byte mask rows), V <= 16384.
@@ -694,7 +724,16 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   if (a.trie.V <= 8192) {
     k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
     if (ev0) cudaEventRecord(ev0, s);
-    k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, 4);
+    switch (g_stream_variant) {
+      case 1:   // one CTA per SM: one producer feeding three consumer groups from a 6-stage ring
+        k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, 4);
+        break;
+      case 2:
+        k_stream<32, 1, 1, 4><<<std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s>>>(a, total, 4);
+        break;
+      default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
+        k_stream<32, 1, 2, 3><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 4);
+    }
   } else {
     k_seed<512, 2><<<a.batch, 1024, stream_smem<64, 2>(), s>>>(a);
     if (ev0) cudaEventRecord(ev0, s);

@@ -279,7 +279,6 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
   if (!sparse_route && ctx->V > 16384)
     return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 is not implemented yet");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
-  if (!sparse_route) ACK(cudaMemsetAsync(ctx->scratch, 0, 3 * (size_t)ctx->maxB * 4, s));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (!ctx->ev.empty() && !sparse_route && ctx->ev_head - ctx->ev_tail < kTimingRing) {
     const int slot = (int)(ctx->ev_head % kTimingRing);
@@ -289,6 +288,7 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
     ++ctx->ev_head;
   }
   int launches = 0;
+  a.sparse_cap = (int)sparse_keys;
   ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s, ev0, ev1, &launches));
   ctx->launches += launches;
   ctx->batch = batch;

@@ -51,6 +51,7 @@ struct StepArgs {
   int32_t theta_rows;
   int32_t counters_on;
   int32_t no_prune;
+  int32_t sparse_cap;   // key capacity of k_sparse's dynamic shared memory
   // state in (null at t = 1: the root, one live beam with score 0)
   const float* score_in;
   const uint32_t* node_in;
@@ -103,6 +104,23 @@ __device__ __forceinline__ float cand_score(float S, float x, float lse) {
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// Debug-build bounds checks (compile with -DXGR_DEBUG): trap with a message on violation.
+#ifdef XGR_DEBUG
+#define XGR_CHECK(cond, ...)                                        \
+  do {                                                              \
+    if (!(cond)) {                                                  \
+      printf("XGR_CHECK failed %s:%d: %s | ", __FILE__, __LINE__, #cond); \
+      printf(__VA_ARGS__);                                          \
+      printf("\n");                                                \
+      __trap();                                                     \
+    }                                                               \
+  } while (0)
+#else
+#define XGR_CHECK(cond, ...) \
+  do {                       \
+  } while (0)
+#endif
+
 // ---- beam state of row b of request req ----------------------------------------------------------
 __device__ __forceinline__ int nlive_of(const StepArgs& a, int req) {
   return a.nlive_in ? a.nlive_in[req] : 1;
@@ -136,6 +154,61 @@ __device__ __forceinline__ uint32_t child_of(const TrieDev& tr, int d, uint32_t 
   const uint16_t* lab = tr.lv[d + 1].label;
   while (lo < hi) {
     uint32_t mid = (lo + hi) >> 1;
+    if (lab[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---- survivor emission: one global atomic per warp ------------------------------------------------
+// Every lane of the warp must call (n may be 0). Returns this lane's first slot in the request's
+// survivor buffer; the warp's total is reserved with a single atomicAdd.
+__device__ __forceinline__ uint32_t warp_reserve(uint32_t n, uint32_t* count) {
+  const int lane = threadIdx.x & 31;
+  uint32_t incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  uint32_t base = 0;
+  if (lane == 31 && total) base = atomicAdd(count, total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  return base + incl - n;
+}
+
+// ---- child id with the parent's (first_child, next first_child, dense slot) already at hand -----
+// Dense: rank directory entry + popcount of the node's 256-bit bitmap block below v, the block
+// fetched with two 16-byte loads. Sparse: binary search of v among the sorted child labels.
+__device__ __forceinline__ uint32_t child_of_pref(const TrieDev& tr, int d, uint32_t fc, uint32_t fcn,
+                                                  int slot, uint32_t v) {
+  const LevelDev& L = tr.lv[d];
+  if (slot >= 0) {
+    const uint32_t* blk = L.bitmap + (size_t)slot * tr.W + ((v >> 8) << 3);
+    uint32_t r = __ldg(L.rankdir + (size_t)slot * tr.R + (v >> 8));
+    uint32_t w[8];
+    const int nw = (int)min((uint32_t)8, (uint32_t)tr.W - ((v >> 8) << 3));
+    if (nw == 8 && ((reinterpret_cast<uintptr_t>(blk) & 15u) == 0)) {
+      const uint4 q0 = __ldg(reinterpret_cast<const uint4*>(blk));
+      const uint4 q1 = __ldg(reinterpret_cast<const uint4*>(blk) + 1);
+      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = i < nw ? __ldg(blk + i) : 0u;
+    }
+    const uint32_t wi = (v >> 5) & 7u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t m = (uint32_t)i < wi ? 0xFFFFFFFFu : ((uint32_t)i == wi ? ((1u << (v & 31)) - 1u) : 0u);
+      r += __popc(w[i] & m);
+    }
+    return fc + r;
+  }
+  uint32_t lo = fc, hi = fcn;
+  const uint16_t* lab = tr.lv[d + 1].label;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
     if (lab[mid] < v) lo = mid + 1; else hi = mid;
   }
   return lo;

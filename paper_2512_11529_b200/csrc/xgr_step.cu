@@ -116,18 +116,6 @@ __device__ __forceinline__ int block_sum_i(int v, int* sh) {
   return r;
 }
 
-// Append `key` to a request's survivor buffer; lanes that arrive together share one atomic.
-__device__ __forceinline__ void emit_key(uint64_t key, uint32_t* count, uint64_t* buf, int cap) {
-  unsigned m = __activemask();
-  int leader = __ffs(m) - 1;
-  int lane = lane_id();
-  uint32_t base = 0;
-  if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
-  base = __shfl_sync(m, base, leader);
-  uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-  if (pos < (uint32_t)cap) buf[pos] = key;
-}
-
 __device__ __forceinline__ void count_add(const StepArgs& a, int idx, unsigned long long v) {
   if (a.counters_on && v) atomicAdd(a.counters + idx, v);
 }
@@ -236,6 +224,58 @@ __device__ __forceinline__ void warp_find_digit_desc(const uint32_t* hist, uint3
   }
 }
 
+__device__ __forceinline__ uint64_t warp_sort_desc_u64(uint64_t v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const uint64_t o = __shfl_xor_sync(0xffffffffu, v, stride);
+      const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
+      v = keep_max ? (o > v ? o : v) : (o < v ? o : v);
+    }
+  }
+  return v;
+}
+
+// Sorts k distinct keys (k <= 1024) descending from `sel` into `out`: each warp sorts a list of
+// 32 in registers (shuffle bitonic) and writes it back in place; a key's final rank is its index
+// in its own list plus, for every other list, the number of greater keys (binary search).
+template <int T>
+__device__ void sort_desc_to(uint64_t* sel, int k, uint64_t* out) {
+  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  const int nl = (k + 31) >> 5;
+  for (int w = warp; w < nl; w += T / 32) {
+    const int p = 32 * w + lane;
+    const uint64_t v = warp_sort_desc_u64(p < k ? sel[p] : 0ull);
+    sel[p] = v;   // padding sorts to the tail as 0 (smaller than every real key)
+  }
+  __syncthreads();
+  for (int p = tid; p < 32 * nl; p += T) {
+    const uint64_t v = sel[p];
+    if (v == 0ull) continue;
+    const int own = p >> 5;
+    int r = p & 31;
+    for (int w = 0; w < nl; ++w) {
+      if (w == own) continue;
+      const uint64_t* lst = sel + 32 * w;
+      // number of keys > v in a descending list of 32: 6 halvings of [0, 32]
+      int lo = 0, hi = 32;
+#pragma unroll
+      for (int it = 0; it < 6; ++it) {
+        if (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (lst[mid] > v) lo = mid + 1; else hi = mid;
+        }
+      }
+      r += lo;
+    }
+    XGR_CHECK(r < k, "sort_desc_to r %d k %d", r, k);
+    out[r] = v;
+  }
+  __syncthreads();
+}
+
 // Selects the k largest of keys[0..n) (distinct keys) into out[0..k), sorted descending.
 // T threads; shared scratch: sel[k], hist[256], misc64[2 * T / 32], misc32[4].
 template <int T>
@@ -281,6 +321,7 @@ __device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* 
       if (tid < 32) warp_find_digit_desc(hist, krem, &misc32[0], &misc32[1]);
       __syncthreads();
       uint32_t d = misc32[0], above = misc32[1];
+      XGR_CHECK(d < 256, "radix digit %u n %d k %d krem %u", d, n, k, krem);
       uint32_t inbin = hist[d];
       krem -= above;
       prefix |= (uint64_t)d << shift;
@@ -302,19 +343,89 @@ __device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* 
     }
   }
   __syncthreads();
-  // rank sort (keys are distinct): out[#keys greater than sel[j]] = sel[j]; one barrier
-  for (int j = tid; j < k; j += T) {
-    const uint64_t v = sel[j];
-    int r = 0;
-    for (int i = 0; i < k; ++i) r += sel[i] > v;
-    out[r] = v;
+  sort_desc_to<T>(sel, k, out);
+}
+
+// Fast top-k of distinct keys in shared memory (used by the per-request select kernels).
+// Threshold without atomics or passes: every thread takes the max of its keys; each warp sorts
+// its 32 maxima (shuffle bitonic) and takes the m-th largest, m = ceil(k / warps); the minimum of
+// those over warps, tau, has >= k keys >= tau (each warp contributes m distinct thread maxima).
+// Keys >= tau (typically ~1.5k) are compacted and rank-sorted. If tau admits too many keys, the
+// exact radix path (block_select_topk) is used instead.
+struct TopkScratch {
+  uint64_t wsel[32];
+  uint32_t n_c;
+  uint64_t m64[64];
+  uint32_t m32[4];
+  uint32_t hist[256];
+};
+
+template <int T>
+__device__ int block_topk_fast(const uint64_t* keys, int n, int k, uint64_t* cand, int cand_cap,
+                               uint64_t* sel, uint64_t* out, TopkScratch& sc) {
+  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  constexpr int NW = T / 32;
+  if (k <= 0) return 0;
+  const int m = (k + NW - 1) / NW;
+  if (n <= 2 * k || m > 32) {
+    block_select_topk<T>(keys, n, k, sel, out, sc.hist, sc.m64, sc.m32);
+    return k;
+  }
+  uint64_t tmax = 0ull;
+  for (int i = tid; i < n; i += T) {
+    const uint64_t v = keys[i];
+    tmax = v > tmax ? v : tmax;
+  }
+  const uint64_t srt = warp_sort_desc_u64(tmax);
+  const uint64_t wm = __shfl_sync(0xffffffffu, srt, m - 1);
+  if (lane == 0) sc.wsel[warp] = wm;
+  if (tid == 0) sc.n_c = 0;
+  __syncthreads();
+  uint64_t tau = sc.wsel[0];
+#pragma unroll
+  for (int w = 1; w < NW; ++w) tau = sc.wsel[w] < tau ? sc.wsel[w] : tau;
+  for (int i = tid; i < n; i += T) {
+    const uint64_t v = keys[i];
+    if (v >= tau) {
+      const unsigned msk = __activemask();
+      const int leader = __ffs(msk) - 1;
+      uint32_t b = 0;
+      if (lane == leader) b = atomicAdd(&sc.n_c, (uint32_t)__popc(msk));
+      b = __shfl_sync(msk, b, leader);
+      const uint32_t p = b + __popc(msk & ((1u << lane) - 1u));
+      if (p < (uint32_t)cand_cap) cand[p] = v;
+    }
   }
   __syncthreads();
+  const int nc = (int)sc.n_c;
+  if (nc > cand_cap) block_select_topk<T>(keys, n, k, sel, out, sc.hist, sc.m64, sc.m32);
+  else block_select_topk<T>(cand, nc, k, sel, out, sc.hist, sc.m64, sc.m32);
+  return k;
+}
+
+// Parent-row trie info for the commit, fetched at kernel start (overlaps the selection work).
+struct ParentInfo {
+  uint32_t fc[kMaxBW];
+  uint32_t fcn[kMaxBW];
+  int32_t slot[kMaxBW];
+};
+
+template <int T>
+__device__ void prefetch_parents(const StepArgs& a, int req, int nl, ParentInfo& pi) {
+  const LevelDev& L = a.trie.lv[a.level];
+  for (int b = threadIdx.x; b < nl; b += T) {
+    const uint32_t node = a.node_in ? a.node_in[(size_t)req * a.BW + b] : 0u;
+    XGR_CHECK(node < (uint32_t)L.n_nodes, "prefetch req %d b %d nl %d node %u n_nodes %lld", req, b, nl, node,
+              (long long)L.n_nodes);
+    pi.fc[b] = L.first_child[node];
+    pi.fcn[b] = L.first_child[node + 1];
+    pi.slot[b] = L.dense_slot ? L.dense_slot[node] : -1;
+  }
 }
 
 // Commit the k selected keys (sorted desc) of request req into the step-t state (a5).
 template <int T>
-__device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k) {
+__device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, const ParentInfo& pi) {
   const int V = a.trie.V;
   const size_t base = (size_t)req * a.BW;
   for (int j = threadIdx.x; j < a.BW; j += T) {
@@ -324,11 +435,12 @@ __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k) {
       uint32_t flat = key_flat(key);
       uint32_t b = flat / (uint32_t)V;
       uint32_t v = flat - b * (uint32_t)V;
-      uint32_t pnode = a.node_in ? a.node_in[base + b] : 0u;
       a.parent_out[base + j] = (int32_t)b;
       a.token_out[base + j] = (int32_t)v;
       a.score_out[base + j] = c;
-      a.node_out[base + j] = child_of(a.trie, a.level, pnode, v);
+      XGR_CHECK(b < (uint32_t)a.BW && v < (uint32_t)V, "commit req %d j %d k %d b %u v %u key %llx", req, j, k, b, v,
+                (unsigned long long)key);
+      a.node_out[base + j] = child_of_pref(a.trie, a.level, pi.fc[b], pi.fcn[b], pi.slot[b], v);
     } else {
       a.parent_out[base + j] = -1;
       a.token_out[base + j] = -1;
@@ -473,13 +585,20 @@ __device__ void sparse_row_main(const StepArgs& a, int req, int b, float S, floa
   }
   int ns = 0;
   const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
-  for (uint32_t k = fc + tid; k < fe; k += T) {
-    uint32_t v = lab[k];
-    float c = cand_score(S, row[v], lse);
-    if (c >= th) {
-      emit_key(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap, a.cap);
-      ++ns;
+  for (uint32_t k0 = fc; k0 < fe; k0 += T) {
+    const uint32_t k = k0 + tid;
+    uint32_t v = 0;
+    float c = -INFINITY;
+    if (k < fe) {
+      v = lab[k];
+      c = cand_score(S, row[v], lse);
     }
+    const bool take = k < fe && c >= th;
+    if (__any_sync(0xffffffffu, take)) {
+      const uint32_t pos = warp_reserve(take ? 1u : 0u, a.surv_count + req);
+      if (take && pos < (uint32_t)a.cap) a.surv[(size_t)req * a.cap + pos] = make_key(c, fbase + v);
+    }
+    ns += take;
   }
   if (a.counters_on) {
     int tot = block_sum_i<T>(ns, s_redi);
@@ -538,22 +657,31 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
   const float xthr = (th == -INFINITY)
                          ? -INFINITY
                          : (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
-  int ns = 0;
+  uint32_t mine = 0u;   // bit 4i+j: element j of x[i] is a candidate (VPT <= 8)
   if (r.tmax >= xthr) {
-    const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
 #pragma unroll
     for (int i = 0; i < VPT; ++i) {
-      float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
+      const float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (((r.nib[i] >> j) & 1u) && xs[j] >= xthr && cand_score(S, xs[j], lse) >= th)
+          mine |= 1u << (4 * i + j);
+    }
+  }
+  const int ns = __popc(mine);
+  if (__any_sync(0xffffffffu, ns > 0)) {
+    const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+    uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const float xs[4] = {r.x[i].x, r.x[i].y, r.x[i].z, r.x[i].w};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        if (((r.nib[i] >> j) & 1u) && xs[j] >= xthr) {
-          float c = cand_score(S, xs[j], lse);
-          if (c >= th) {
-            uint32_t v = 4u * (uint32_t)(i * T + tid) + j;
-            emit_key(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap,
-                     a.cap);
-            ++ns;
-          }
+        if ((mine >> (4 * i + j)) & 1u) {
+          const uint32_t v = 4u * (uint32_t)(i * T + tid) + j;
+          if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, xs[j], lse), fbase + v);
+          ++pos;
         }
       }
     }
@@ -569,11 +697,11 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
 // ---------------------------------------------------------------------------------------------
 template <int T>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) uint64_t s_keys[];  // [cap]
+  extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
+  uint64_t* s_cand = s_keys + a.cap;
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint64_t s_m64[2 * (T / 32)];
-  __shared__ uint32_t s_m32[4];
+  __shared__ TopkScratch s_sc;
+  __shared__ ParentInfo s_pi;
   const int req = blockIdx.x, tid = threadIdx.x;
   const uint32_t n = a.surv_count[req];
   if (n > (uint32_t)a.cap) {
@@ -587,9 +715,10 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   const int k = min((int)n, a.BW);
   const uint64_t* src = a.surv + (size_t)req * a.cap;
   for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
+  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
   __syncthreads();
-  block_select_topk<T>(s_keys, (int)n, k, s_sel, s_out, s_hist, s_m64, s_m32);
-  commit<T>(a, req, s_out, k);
+  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  commit<T>(a, req, s_out, k, s_pi);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -629,12 +758,14 @@ __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, i
 
 template <int T>
 __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs a) {
-  __shared__ uint64_t s_sel[kMaxBW];
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ uint32_t s_hist[256];
   __shared__ uint32_t s_m32[4];
+  __shared__ ParentInfo s_pi;
   const int req = blockIdx.x, tid = threadIdx.x;
   if (!a.ovf[req]) return;
   const int nl = nlive_of(a, req);
+  prefetch_parents<T>(a, req, nl, s_pi);
   const float th = theta_value(a.theta[req]);
   const uint64_t klo = (uint64_t)a.theta[req] << 32;
   const int k = a.BW;  // overflow => more than cap >= BW candidates >= theta
@@ -689,26 +820,8 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
   }
   __syncthreads();
   const int kk = min(k, (int)s_m32[2]);
-  int P = 1;
-  while (P < kk) P <<= 1;
-  for (int i = kk + tid; i < P; i += T) s_sel[i] = 0ull;
-  __syncthreads();
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < P / 2; i += T) {
-        int lo = 2 * i - (i & (stride - 1));
-        int hi = lo + stride;
-        bool desc = ((lo & size) == 0);
-        uint64_t x = s_sel[lo], y = s_sel[hi];
-        if ((x < y) == desc) {
-          s_sel[lo] = y;
-          s_sel[hi] = x;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  commit<T>(a, req, s_sel, kk);
+  sort_desc_to<T>(s_sel, kk, s_out);
+  commit<T>(a, req, s_out, kk, s_pi);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -719,11 +832,12 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
 // ---------------------------------------------------------------------------------------------
 template <int T, bool ROOT>
 __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) uint64_t s_keys[];  // [rows * max_children]
+  extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
+  uint64_t* s_cand = s_dynk;
+  uint64_t* s_keys = s_dynk + 2 * kMaxBW;
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint64_t s_m64[2 * (T / 32)];
-  __shared__ uint32_t s_m32[4];
+  __shared__ TopkScratch s_sc;
+  __shared__ ParentInfo s_pi;
   __shared__ float s_red[T / 32], s_red2[T / 32];
   __shared__ uint32_t s_count, s_nbig;
   __shared__ int32_t s_big[kMaxBW];
@@ -736,6 +850,7 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
     s_count = 0;
     s_nbig = 0;
   }
+  prefetch_parents<T>(a, req, nl, s_pi);
   __syncthreads();
   if (ROOT) {
     for (int b = 0; b < nl; ++b) {
@@ -793,6 +908,7 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
       const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
       const uint32_t base = atomicAdd(&s_count, (uint32_t)cnt);
+      XGR_CHECK(base + cnt <= (uint32_t)a.sparse_cap, "sparse keys base %u cnt %d cap %d", base, cnt, a.sparse_cap);
 #pragma unroll
       for (int k = 0; k < kSmall; ++k)
         if (k < cnt) s_keys[base + k] = make_key(cand_score(S, xv[k], lse), (uint32_t)b * V + vv[k]);
@@ -829,8 +945,8 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
   const int n = (int)s_count;
   if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
   const int k = min(n, a.BW);
-  block_select_topk<T>(s_keys, n, k, s_sel, s_out, s_hist, s_m64, s_m32);
-  commit<T>(a, req, s_out, k);
+  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  commit<T>(a, req, s_out, k, s_pi);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -984,13 +1100,13 @@ cudaError_t configure_kernels(int cap) {
   cudaError_t e = configure_stream_kernels();
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(cap * sizeof(uint64_t)));
+                           (int)((cap + 2 * kMaxBW) * sizeof(uint64_t)));
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_sparse<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(kSparseCap * sizeof(uint64_t)));
+                           (int)((kSparseCap + 2 * kMaxBW) * sizeof(uint64_t)));
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_sparse<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(kSparseCap * sizeof(uint64_t)));
+                              (int)((kSparseCap + 2 * kMaxBW) * sizeof(uint64_t)));
 }
 
 bool stream_supported(int V);
@@ -1001,7 +1117,7 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
   if (sparse_route) {
-    size_t smem = (size_t)sparse_keys * sizeof(uint64_t);
+    size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
     if (rows == 1) k_sparse<512, true><<<a.batch, 512, smem, s>>>(a);
     else k_sparse<512, false><<<a.batch, 512, smem, s>>>(a);
     ++*launches;
@@ -1009,14 +1125,18 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   }
   const int V = a.trie.V;
   if (stream_supported(V)) {
-    e = launch_stream(a, rows, s, ev0, ev1, launches);
+    e = launch_stream(a, rows, s, ev0, ev1, launches);   // k_seed resets theta/count/ovf
+  } else if ((e = cudaMemsetAsync(a.theta, 0, (size_t)a.batch * 4, s)) != cudaSuccess ||
+             (e = cudaMemsetAsync(a.surv_count, 0, (size_t)a.batch * 4, s)) != cudaSuccess ||
+             (e = cudaMemsetAsync(a.ovf, 0, (size_t)a.batch * 4, s)) != cudaSuccess) {
+    return e;
   } else if (V <= 2048) e = launch_dense<128, 4>(a, rows, s, ev0, ev1, launches);
   else if (V <= 4096) e = launch_dense<256, 4>(a, rows, s, ev0, ev1, launches);
   else if (V <= 8192) e = launch_dense<256, 8>(a, rows, s, ev0, ev1, launches);
   else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s, ev0, ev1, launches);
   else return cudaErrorNotSupported;
   if (e != cudaSuccess) return e;
-  k_select<512><<<a.batch, 512, (size_t)a.cap * sizeof(uint64_t), s>>>(a);
+  k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
   k_fallback<512><<<a.batch, 512, 0, s>>>(a);
   *launches += 2;
   return cudaGetLastError();

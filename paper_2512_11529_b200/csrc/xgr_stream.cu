@@ -85,16 +85,6 @@ __device__ __forceinline__ float wsum(float v) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ void emit(uint64_t key, uint32_t* count, uint64_t* buf, int cap) {
-  unsigned m = __activemask();
-  int leader = __ffs(m) - 1;
-  int lane = threadIdx.x & 31;
-  uint32_t base = 0;
-  if (lane == leader) base = atomicAdd(count, (uint32_t)__popc(m));
-  base = __shfl_sync(m, base, leader);
-  uint32_t pos = base + __popc(m & ((1u << lane) - 1u));
-  if (pos < (uint32_t)cap) buf[pos] = key;
-}
 __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -152,7 +142,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
   float* s_row = s_dyn;                                                   // [R0][32*CTR]
   uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dyn + R0 * 32 * CTR);  // [R0][CTR]
   __shared__ __align__(8) uint64_t bar;
-  __shared__ int r_kind[R0], r_slot[R0];
+  __shared__ int r_kind[R0], r_slot[R0], r_ok[R0];
   __shared__ float r_S[R0];
   __shared__ float g_max[NT / 32], g_sum[NT / 32];
   __shared__ float b_red[2][NT / 32];
@@ -179,6 +169,8 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
   if (tid == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    a.surv_count[req] = 0u;   // this step's per-request scratch (read by later kernels only)
+    a.ovf[req] = 0u;
   }
   for (int i = tid; i < R0 * CTR; i += NT) s_msk[i] = 0u;
   __syncthreads();
@@ -265,13 +257,17 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 #pragma unroll
     for (int i = 0; i < 32; ++i) c[i] = -INFINITY;
   }
+  if (lt == 0) r_ok[g] = kind;   // this seed row is dense, live and finite
   if (a.counters_on) {
     int lc = __reduce_add_sync(0xffffffffu, r_kind[g] ? __popc(wraw) : 0);
     if (lane == 0 && lc) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
   }
 
-  // block-wide (union of the seed rows) threshold: histogram of hi0 - c over [0, 16) in 1024
-  // bins of 1/64, cumulative count from the top, then an exact count verifies the bound.
+  // block-wide (union of the seed rows) threshold. Every thread's best candidate cmaxv; each warp
+  // sorts its 32 (shuffle bitonic) and takes the m-th largest, m = ceil(BW / warps); the minimum
+  // over warps, tau0, has >= BW candidates >= tau0. The candidates >= tau0 (a few hundred) are
+  // compacted and the exact BW-th largest among them is theta (>= BW candidates >= theta, so
+  // theta <= the request's true BW-th best score).
   auto bmax = [&](float x) {
     x = wmax(x);
     if (lane == 0) b_red[0][tid >> 5] = x;
@@ -290,63 +286,117 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
     for (int i = 0; i < NT / 32; ++i) r += b_cnt[buf][i];
     return r;
   };
-  const float hi0 = bmax(cmaxv);
-  const int total = bcnt(nleg, 0);
   float lo = -INFINITY;
-  if (!a.no_prune && total >= BW && hi0 > -INFINITY) {
-    constexpr int NB = NT;            // one bin per thread
-    constexpr float kRange = 16.0f;
-    constexpr float kScale = NB / kRange;
-    uint32_t* hist = reinterpret_cast<uint32_t*>(s_row);   // the rows are in registers now
-    __syncthreads();
-    hist[tid] = 0u;
-    __syncthreads();
+  const int total = bcnt(nleg, 0);   // (its barrier also publishes r_ok)
+  int nrows_ok = 0;
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float dd = (hi0 - c[i]) * kScale;
-      if (dd < (float)NB) atomicAdd(&hist[(int)dd], 1u);   // -inf / NaN never pass
+  for (int r = 0; r < R0; ++r) nrows_ok += r_ok[r];
+  const int nws = nrows_ok * (CTR / 32);   // warps holding a usable seed row
+  const int mth = nws ? (BW + nws - 1) / nws : 33;
+  if (!a.no_prune && total >= BW && mth <= 32) {
+    // warp bitonic sort (descending) of the thread maxima
+    float v = cmaxv;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+        const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
+        v = keep_max ? fmaxf(v, o) : fminf(v, o);
+      }
     }
-    __syncthreads();
-    // inclusive scan of the bins (bin t = thread t): warp scan, then warp offsets
-    uint32_t v = hist[tid];
+    const float wmth = kind ? __shfl_sync(0xffffffffu, v, mth - 1) : INFINITY;
+    const float tau0 = -bmax(-wmth);   // block min over the usable warps
+    if (tau0 > -INFINITY) {
+      float* cvals = s_row;            // the rows are in registers now
+      if (tid == 0) b_cnt[1][0] = 0;
+      __syncthreads();
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += y;
-    }
-    if (lane == 31) b_cnt[1][tid >> 5] = (int)v;
-    __syncthreads();
-    uint32_t off = 0;
-    for (int i = 0; i < (tid >> 5); ++i) off += (uint32_t)b_cnt[1][i];
-    v += off;
-    const uint32_t prev = v - hist[tid];
-    if (tid == 0) b_red[1][0] = -1.0f;
-    __syncthreads();
-    if (v >= (uint32_t)BW && prev < (uint32_t)BW) b_red[1][0] = (float)tid;
-    __syncthreads();
-    const float tb = b_red[1][0];
-    if (tb >= 0.0f) {
-      // every value counted in bins <= tb has c > hi0 - (tb + 1) / kScale; half a bin of margin
-      const float cand = hi0 - (tb + 1.5f) / kScale;
-      int n = 0;
+      for (int i = 0; i < 32; ++i) {
+        if (c[i] >= tau0) {
+          const unsigned msk = __activemask();
+          const int leader = __ffs(msk) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(&b_cnt[1][0], __popc(msk));
+          base = __shfl_sync(msk, base, leader);
+          const int p = base + __popc(msk & ((1u << lane) - 1u));
+          if (p < 8192) cvals[p] = c[i];
+        }
+      }
+      __syncthreads();
+      const int n0 = b_cnt[1][0];
+      lo = tau0;
+      if (n0 <= 8192) {
+        // exact BW-th largest of the compacted candidates: MSB radix select on orderable bits
+        uint32_t* hist = reinterpret_cast<uint32_t*>(s_row + 8192);
+        uint32_t prefix = 0u, pmask = 0u;
+        int krem = BW;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+          if (tid < 256) hist[tid] = 0u;
+          __syncthreads();
+          for (int j = tid; j < n0; j += NT) {
+            const uint32_t u = f2o(cvals[j]);
+            if ((u & pmask) == prefix) atomicAdd(&hist[(u >> shift) & 0xFFu], 1u);
+          }
+          __syncthreads();
+          if (tid < 32) {
+            // lane l owns bins 255-8l .. 248-8l; find the digit where the count from the top reaches krem
+            uint32_t cc[8], sum = 0;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) n += c[i] >= cand;
-      if (bcnt(n, 0) >= BW) lo = cand;
+            for (int q = 0; q < 8; ++q) {
+              cc[q] = hist[255 - 8 * lane - q];
+              sum += cc[q];
+            }
+            uint32_t incl = sum;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += y;
+            }
+            const uint32_t excl = incl - sum;
+            if (excl < (uint32_t)krem && incl >= (uint32_t)krem) {
+              uint32_t acc = excl;
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                if (acc + cc[q] >= (uint32_t)krem) {
+                  b_cnt[1][1] = 255 - 8 * lane - q;
+                  b_cnt[1][2] = (int)acc;
+                  break;
+                }
+                acc += cc[q];
+              }
+            }
+          }
+          __syncthreads();
+          const uint32_t dgt = (uint32_t)b_cnt[1][1];
+          krem -= b_cnt[1][2];
+          prefix |= dgt << shift;
+          pmask |= 0xFFu << shift;
+          __syncthreads();
+        }
+        lo = o2f(prefix);   // the BW-th largest candidate value (exactly)
+      }
     }
   }
   if (tid == 0) a.theta[req] = lo > -INFINITY ? f2o(lo) : 0u;
-  // emit the seed rows' candidates >= theta (lo == -inf: every legal candidate)
-  int ns = 0;
+  // emit the seed rows' candidates >= theta (lo == -inf: every legal candidate); one global
+  // atomic per warp reserves the slots
+  uint32_t mine = 0u;
   if (kind && cmaxv >= lo) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) mine |= ((((wm >> i) & 1u) && c[i] >= lo) ? 1u : 0u) << i;
+  }
+  const int ns = __popc(mine);
+  if (__any_sync(0xffffffffu, ns > 0)) {
     const uint32_t fbase = (uint32_t)g * (uint32_t)V;
-    uint32_t* cnt = a.surv_count + req;
     uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+    uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      if (((wm >> i) & 1u) && c[i] >= lo) {
+      if ((mine >> i) & 1u) {
         const uint32_t v = 32u * lt + 4u * (((i >> 2) + lt) & 7) + (i & 3);
-        emit(make_key(c[i], fbase + v), cnt, sbuf, a.cap);
-        ++ns;
+        if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(c[i], fbase + v);
+        ++pos;
       }
     }
   }
@@ -560,10 +610,19 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (!finite) continue;
       if (!(cand_score(S, M, lse) >= th)) continue;
       const uint32_t fbase = (uint32_t)b * (uint32_t)V;
-      for (uint32_t q = fc + lt; q < fe; q += GT) {
-        const uint32_t v = lab[q];
-        const float c = cand_score(S, row[v], lse);
-        if (c >= th) emit(make_key(c, fbase + v), a.surv_count + req, a.surv + (size_t)req * a.cap, a.cap);
+      for (uint32_t q0 = fc; q0 < fe; q0 += GT) {
+        const uint32_t q = q0 + lt;
+        uint32_t v = 0;
+        float c = -INFINITY;
+        if (q < fe) {
+          v = lab[q];
+          c = cand_score(S, row[v], lse);
+        }
+        const bool take = q < fe && c >= th;
+        if (__any_sync(0xffffffffu, take)) {
+          const uint32_t pos = warp_reserve(take ? 1u : 0u, a.surv_count + req);
+          if (take && pos < (uint32_t)a.cap) a.surv[(size_t)req * a.cap + pos] = make_key(c, fbase + v);
+        }
       }
       continue;
     }
@@ -638,25 +697,15 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
     }
-    int ns = 0;
-    const uint32_t fbase = (uint32_t)b * (uint32_t)V;
-    uint32_t* cnt = a.surv_count + req;
-    uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+    // select this thread's candidates (bit e of `mine`), then one atomic per warp reserves slots
+    uint64_t mine = 0ull;
     if (th > -INFINITY) {
       // conservative pre-filter on x (the exact test c >= theta follows); illegal x are -inf
       const float xthr = (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
       if (tmax >= xthr) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          if (x[e] >= xthr) {
-            const float c = cand_score(S, x[e], lse);
-            if (c >= th) {
-              const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
-              emit(make_key(c, fbase + v), cnt, sbuf, a.cap);
-              ++ns;
-            }
-          }
-        }
+        for (int e = 0; e < EPT; ++e)
+          if (x[e] >= xthr && cand_score(S, x[e], lse) >= th) mine |= 1ull << e;
       }
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
@@ -665,14 +714,21 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
 #pragma unroll
       for (int i = 0; i < NF4; ++i) {
         const uint32_t q4 = (uint32_t)(i * GT + lt);
-        const uint32_t nb = (4 * q4 < (uint32_t)V) ? (__ldg(gm + i * (GT / 8)) >> nsh) : 0u;
+        const uint32_t nb = (4 * q4 < (uint32_t)V) ? ((__ldg(gm + i * (GT / 8)) >> nsh) & 0xFu) : 0u;
+        mine |= (uint64_t)nb << (4 * i);
+      }
+    }
+    const int ns = __popcll(mine);
+    if (__any_sync(0xffffffffu, ns > 0)) {
+      const uint32_t fbase = (uint32_t)b * (uint32_t)V;
+      uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+      uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if ((nb >> j) & 1u) {
-            const float c = cand_score(S, x[4 * i + j], lse);
-            emit(make_key(c, fbase + 4u * q4 + j), cnt, sbuf, a.cap);
-            ++ns;
-          }
+      for (int e = 0; e < EPT; ++e) {
+        if ((mine >> e) & 1ull) {
+          const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
+          if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, x[e], lse), fbase + v);
+          ++pos;
         }
       }
     }

@@ -358,9 +358,16 @@ def _full(xgr, name, check_reqs, sigma=2.0):
 def test_c2_full_size_sampled(xgr):
     out, stats, bs = _full(xgr, "C2", [0, 17, 63])
     assert np.all(out["n_live"] == 128)
+    # the threshold seed keeps survivors near BW: no request needs the overflow fallback
+    cnt = bs.counters()
+    assert cnt["overflow"] == 0, cnt
+    assert cnt["survivors"] <= 8 * 128 * 64, cnt
 
 
 @pytest.mark.slow
 def test_c3_full_size_sampled(xgr):
     out, stats, bs = _full(xgr, "C3", [0, 101, 255])
     assert np.all(out["n_live"] == 256)
+    cnt = bs.counters()
+    assert cnt["overflow"] == 0, cnt
+    assert cnt["survivors"] <= 8 * 256 * 256, cnt

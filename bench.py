@@ -278,7 +278,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             step_dense = statistics.median(per_step[dense_steps[0] - 1]) if dense_steps else None
             tr = committed_traffic()
             res["roofline"] = {
-                "bound": "hbm", "kernel": "k_main (dense step: masked log-softmax + score add + pruned emit)",
+                "bound": "hbm", "kernel": "k_stream (dense step: TMA row stream, masked log-softmax, score add, pruned emit)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src == "measured" else "fallback 6.65 TB/s",
                 "traffic": (tr or {}).get("dram_bytes_per_launch"),

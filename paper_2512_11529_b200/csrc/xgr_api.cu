@@ -6,6 +6,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -289,6 +290,8 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
   }
   int launches = 0;
   a.sparse_cap = (int)sparse_keys;
+  static const int dbg_flags = getenv("XGR_DEBUG_FLAGS") ? atoi(getenv("XGR_DEBUG_FLAGS")) : 0;
+  a.dbg = dbg_flags;
   ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s, ev0, ev1, &launches));
   ctx->launches += launches;
   ctx->batch = batch;

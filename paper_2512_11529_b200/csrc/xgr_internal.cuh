@@ -52,6 +52,7 @@ struct StepArgs {
   int32_t counters_on;
   int32_t no_prune;
   int32_t sparse_cap;   // key capacity of k_sparse's dynamic shared memory
+  int32_t dbg;          // XGR_DEBUG_FLAGS (experiments only; 0 in production)
   // state in (null at t = 1: the root, one live beam with score 0)
   const float* score_in;
   const uint32_t* node_in;

@@ -575,6 +575,23 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     return r;
   };
   int it = 0;   // this group's dense-row count: parity selects the partials buffer
+  // Deferred survivor emission: a warp reserves its slots with one atomicAdd whose result is
+  // consumed only when the warp next emits (or at the end), so the atomic's round trip overlaps
+  // the following rows instead of stalling the group (at most 2 pending keys per lane).
+  uint32_t pend_res = 0u, pend_off = 0u;
+  int pend_n = 0, pend_req = -1;   // pend_req is warp-uniform; -1: nothing pending
+  uint64_t pend_k0 = 0ull, pend_k1 = 0ull;
+  auto flush = [&]() {
+    if (pend_req >= 0) {
+      const uint32_t base = __shfl_sync(0xffffffffu, pend_res, 31) + pend_off;
+      uint64_t* sbuf = a.surv + (size_t)pend_req * a.cap;
+      if (!(a.dbg & 8)) {
+        if (pend_n > 0 && base < (uint32_t)a.cap) sbuf[base] = pend_k0;
+        if (pend_n > 1 && base + 1 < (uint32_t)a.cap) sbuf[base + 1] = pend_k1;
+      }
+      pend_req = -1;
+    }
+  };
   for (int k = g;; k += G) {
     const int w = blockIdx.x + k * gridDim.x;
     if (w >= total) break;
@@ -704,8 +721,16 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       const float xthr = (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
       if (tmax >= xthr) {
 #pragma unroll
-        for (int e = 0; e < EPT; ++e)
-          if (x[e] >= xthr && cand_score(S, x[e], lse) >= th) mine |= 1ull << e;
+        for (int i = 0; i < NF4; ++i) {
+          const float m4 = fmaxf(fmaxf(x[4 * i], x[4 * i + 1]), fmaxf(x[4 * i + 2], x[4 * i + 3]));
+          if (m4 >= xthr) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int e = 4 * i + j;
+              if (x[e] >= xthr && cand_score(S, x[e], lse) >= th) mine |= 1ull << e;
+            }
+          }
+        }
       }
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
@@ -719,17 +744,49 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       }
     }
     const int ns = __popcll(mine);
-    if (__any_sync(0xffffffffu, ns > 0)) {
+    if ((a.dbg & 1) == 0 && __any_sync(0xffffffffu, ns > 0)) {
+      flush();
       const uint32_t fbase = (uint32_t)b * (uint32_t)V;
-      uint64_t* sbuf = a.surv + (size_t)req * a.cap;
-      uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
+      if (__any_sync(0xffffffffu, ns > 2)) {
+        // many candidates in one lane (weak theta): reserve and write synchronously
+        uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+        uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        if ((mine >> e) & 1ull) {
-          const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
-          if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, x[e], lse), fbase + v);
-          ++pos;
+        for (int e = 0; e < EPT; ++e) {
+          if ((mine >> e) & 1ull) {
+            const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
+            if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, x[e], lse), fbase + v);
+            ++pos;
+          }
         }
+      } else {
+        int q = 0;
+#pragma unroll
+        for (int i = 0; i < NF4; ++i) {
+          const uint32_t nb = (uint32_t)(mine >> (4 * i)) & 0xFu;
+          if (nb) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              if ((nb >> j) & 1u) {
+                const uint32_t v = 4u * (uint32_t)(i * GT + lt) + j;
+                const uint64_t key = make_key(cand_score(S, x[4 * i + j], lse), fbase + v);
+                if (q == 0) pend_k0 = key; else pend_k1 = key;
+                ++q;
+              }
+            }
+          }
+        }
+        uint32_t incl = (uint32_t)ns;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane == 31) pend_res = (a.dbg & 2) ? 0u : atomicAdd(a.surv_count + req, total);
+        pend_off = incl - (uint32_t)ns;
+        pend_n = ns;
+        pend_req = req;
       }
     }
     if (a.counters_on) {
@@ -737,6 +794,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
     }
   }
+  flush();
 }
 
 template <int EPT, int NS>
@@ -746,6 +804,7 @@ static size_t stream_smem() {
 
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
+static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
 
 template <typename K>
 static cudaError_t opt_in(K k, size_t smem) {
@@ -764,6 +823,8 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 1, 4>, stream_smem<32, 1>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<64, 2, 3>, stream_smem<64, 3>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 4>, stream_smem<32, 4>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_seed<256, 2>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
@@ -778,17 +839,19 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
   if (a.trie.V <= 8192) {
-    k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+    const int seeded = g_seed_rows == 2 ? 2 : 4;
+    if (seeded == 2) k_seed<256, 2><<<a.batch, 512, stream_smem<32, 2>(), s>>>(a);
+    else k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
     if (ev0) cudaEventRecord(ev0, s);
     switch (g_stream_variant) {
       case 1:   // one CTA per SM: one producer feeding three consumer groups from a 6-stage ring
-        k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, 4);
+        k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, seeded);
         break;
       case 2:
-        k_stream<32, 1, 1, 4><<<std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s>>>(a, total, 4);
+        k_stream<32, 1, 1, 4><<<std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s>>>(a, total, seeded);
         break;
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
-        k_stream<32, 1, 2, 3><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 4);
+        k_stream<32, 1, 2, 3><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, seeded);
     }
   } else {
     k_seed<512, 2><<<a.batch, 1024, stream_smem<64, 2>(), s>>>(a);

@@ -133,8 +133,8 @@ def measured_peaks():
 
 
 def committed_traffic():
-    """dram bytes per launch of k_main from the committed ncu --set full summary, if any."""
-    p = os.path.join(ROOT, "profiles", "ncu_k_main_traffic.json")
+    """dram bytes per launch of k_stream from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_k_stream_traffic.json")
     try:
         with open(p) as f:
             return json.load(f)

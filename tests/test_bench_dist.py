@@ -1,0 +1,65 @@
+"""Multi-rank host logic of bench.py with the gloo backend on CPU (world size 2): per-rank work
+plans are disjoint (weak scaling over requests), the max-over-ranks reduction, barriers, and the
+reference arm's rank-0-only rule. No GPU needed."""
+import os
+import socket
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    import bench
+    from synth import config
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = config("C3")
+    plan = bench.rank_plan(cfg, rank, world)
+    seeds = bench.step_seeds(plan, cfg["nd"])
+    t = bench.max_over_ranks(float(10 + rank), world, device=torch.device("cpu"))
+    bench.barrier(world)
+    q.put((rank, plan, seeds, t, bench.candidates_per_pass(cfg, plan["batch"])))
+    dist.destroy_process_group()
+
+
+def test_two_ranks_gloo():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (r0, p0, s0, t0, c0), (r1, p1, s1, t1, c1) = res
+    assert t0 == t1 == 11.0                     # max over ranks
+    assert set(s0).isdisjoint(s1)               # distinct logit seeds per rank
+    assert p0["requests"][1] == p1["requests"][0]   # contiguous, disjoint request ranges
+    assert p0["batch"] == p1["batch"] == 256 and c0 == c1 == 256 * (1 + 256 * 2) * 8192
+
+
+def test_reference_arm_nonzero_rank_exits(monkeypatch):
+    sys.path.insert(0, ROOT)
+    import bench
+    monkeypatch.setenv("RANK", "1")
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    assert bench.main(["--impl", "reference"]) == 0

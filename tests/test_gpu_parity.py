@@ -371,3 +371,12 @@ def test_c3_full_size_sampled(xgr):
     cnt = bs.counters()
     assert cnt["overflow"] == 0, cnt
     assert cnt["survivors"] <= 8 * 256 * 256, cnt
+
+
+@pytest.mark.slow
+def test_c4_full_size_sampled(xgr):
+    """C4 (V = 16384, BW = 512, ND = 4, 100M items): the dense step runs the V = 16384 kernels."""
+    out, stats, bs = _full(xgr, "C4", [0, 511])
+    assert np.all(out["n_live"] == 512)
+    cnt = bs.counters()
+    assert cnt["overflow"] == 0, cnt

@@ -202,7 +202,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             bs.step(logits[t])
             if evs:
                 evs[t + 1].record(stream)
-        bs.finalize(on_device=True, out=out)
+        # finalize (a6) is fused into the last step's commit: the item tuples, ranks and scores
+        # are in device memory now (bs.outputs_view()); this call only ends the batch
+        bs.finalize_in_place()
         if evs:
             evs[ND + 1].record(stream)
 

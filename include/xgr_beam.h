@@ -110,6 +110,10 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
                          int64_t ld, void* stream);
 
 /* After exactly nd steps: item tuples of the final beams, in slot order (score descending).
+ * The last step's kernels already wrote them into ctx-owned device buffers (fused finalize);
+ * this call copies them out (device->device or device->host) and resets the ctx. With
+ * outputs_on_device != 0 and all output pointers NULL it only resets: read the results in place
+ * through xgr_beam_outputs (valid until the next batch's last step).
  * tokens [batch][BW][nd] int32, item_rank [batch][BW] int64 (rank in the sorted de-duplicated
  * item list), score [batch][BW] fp32 (sum of the per-step log-probabilities), n_live [batch].
  * Dead slots (n_live <= j < BW): tokens/item_rank -1, score -inf. Any output pointer may be NULL.
@@ -174,6 +178,11 @@ xgr_status xgr_beam_counters(xgr_ctx* ctx, uint64_t* out, void* stream);
  * (every live row, whole V). Host outputs; synchronous; not for the timed path. */
 xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_bytes,
                             int64_t* legal_candidates, void* stream);
+
+/* Device pointers to the ctx-owned final outputs (same layouts as xgr_beam_finalize): written by
+ * the last step of every batch, valid until the next batch's last step. */
+xgr_status xgr_beam_outputs(const xgr_ctx* ctx, const int32_t** tokens, const int64_t** item_rank,
+                            const float** score, const int32_t** n_live);
 
 /* Host-side count of the kernels this ctx has launched since init (step and finalize). */
 int64_t xgr_beam_launch_count(const xgr_ctx* ctx);

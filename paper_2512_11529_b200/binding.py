@@ -31,7 +31,7 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_finaliz
            "xgr_beam_destroy", "xgr_last_error", "xgr_abi_version", "xgr_beam_view",
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
-           "xgr_beam_kernel_times"]
+           "xgr_beam_kernel_times", "xgr_beam_outputs"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -71,6 +71,7 @@ def _load():
         "xgr_beam_counters": [VP, VP, VP],
         "xgr_beam_account": [VP, VP, VP, VP, VP],
         "xgr_beam_kernel_times": [VP, VP, VP, I32, VP],
+        "xgr_beam_outputs": [VP, P(VP), P(VP), P(VP), P(VP)],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -226,6 +227,11 @@ class BeamSearch:
         self.batch = b
         self.t += 1
 
+    def finalize_in_place(self, stream=None):
+        """Ends the batch without copying: results stay in the ctx buffers (outputs_view())."""
+        _check(xgr_beam_finalize(self.ctx, None, None, None, None, 1, self._stream(stream)))
+        self.t = 0
+
     def finalize(self, on_device: bool = True, stream=None, out=None):
         """Returns dict(tokens [B][BW][ND] int32, item_rank [B][BW] int64, score [B][BW] fp32,
         n_live [B] int32); CUDA tensors if on_device else numpy arrays (pinned copies)."""
@@ -293,6 +299,17 @@ class BeamSearch:
         out = np.zeros(XGR_NUM_COUNTERS, dtype=np.uint64)
         _check(lib.xgr_beam_counters(self.ctx, out.ctypes.data, self._stream()))
         return dict(zip(COUNTER_NAMES, (int(v) for v in out)))
+
+    def outputs_view(self):
+        """Zero-copy CUDA views of the ctx-owned final outputs (written by the last step)."""
+        t, r, sc, nl = (ctypes.c_void_p() for _ in range(4))
+        _check(lib.xgr_beam_outputs(self.ctx, ctypes.byref(t), ctypes.byref(r), ctypes.byref(sc),
+                                    ctypes.byref(nl)))
+        B, BW = self.batch, self.bw
+        return {"tokens": _view(t.value, (B, BW, self.nd), "<i4", self.device),
+                "item_rank": _view(r.value, (B, BW), "<i8", self.device),
+                "score": _view(sc.value, (B, BW), "<f4", self.device),
+                "n_live": _view(nl.value, (B,), "<i4", self.device)}
 
     def launch_count(self) -> int:
         return int(lib.xgr_beam_launch_count(self.ctx))

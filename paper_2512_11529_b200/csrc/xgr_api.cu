@@ -17,11 +17,6 @@ namespace xgr {
 cudaError_t configure_kernels(int cap);
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
-cudaError_t launch_finalize(int batch, int BW, int nd, const int32_t* const* parent_hist,
-                            const int32_t* const* token_hist, const uint32_t* node,
-                            const float* score, const int32_t* nlive, int32_t* tokens,
-                            int64_t* item_rank, float* out_score, int32_t* out_nlive,
-                            cudaStream_t s);
 cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
                             int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s);
 cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched,
@@ -271,6 +266,15 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
   a.lse = ctx->lse;
   a.flags = ctx->flags;
   a.counters = ctx->counters;
+  a.nd = ctx->nd;
+  a.phist = ctx->d_phist;
+  a.thist = ctx->d_thist;
+  if (t == ctx->nd) {   // the last step's commit also writes the final items (fused finalize)
+    a.fin_tokens = ctx->out_tokens;
+    a.fin_rank = ctx->out_rank;
+    a.fin_score = ctx->out_score;
+    a.fin_nlive = ctx->out_nlive;
+  }
 
   const int rows_live = need_rows;  // upper bound on live rows of any request this step
   const int64_t maxc = ctx->trie.lv[t - 1].max_children;
@@ -311,14 +315,14 @@ xgr_status xgr_beam_finalize(xgr_ctx* ctx, int32_t* tokens, int64_t* item_rank, 
   const int B = ctx->batch, BW = ctx->BW, nd = ctx->nd;
   const size_t nb = (size_t)B * BW;
   xgr_status st = XGR_OK;
-  ctx->launches += 1;
+  // the final items were written by the last step's commit into the ctx's output buffers
   if (outputs_on_device) {
-    ACK(launch_finalize(B, BW, nd, ctx->d_phist, ctx->d_thist, ctx->node[fin], ctx->score[fin],
-                        ctx->nlive[fin], tokens, item_rank, score, n_live, s));
+    const cudaMemcpyKind k = cudaMemcpyDeviceToDevice;
+    if (tokens) ACK(cudaMemcpyAsync(tokens, ctx->out_tokens, nb * nd * 4, k, s));
+    if (item_rank) ACK(cudaMemcpyAsync(item_rank, ctx->out_rank, nb * 8, k, s));
+    if (score) ACK(cudaMemcpyAsync(score, ctx->out_score, nb * 4, k, s));
+    if (n_live) ACK(cudaMemcpyAsync(n_live, ctx->out_nlive, (size_t)B * 4, k, s));
   } else {
-    ACK(launch_finalize(B, BW, nd, ctx->d_phist, ctx->d_thist, ctx->node[fin], ctx->score[fin],
-                        ctx->nlive[fin], ctx->out_tokens, ctx->out_rank, ctx->out_score,
-                        ctx->out_nlive, s));
     if (tokens) ACK(cudaMemcpyAsync(tokens, ctx->out_tokens, nb * nd * 4, cudaMemcpyDeviceToHost, s));
     if (item_rank) ACK(cudaMemcpyAsync(item_rank, ctx->out_rank, nb * 8, cudaMemcpyDeviceToHost, s));
     if (score) ACK(cudaMemcpyAsync(score, ctx->out_score, nb * 4, cudaMemcpyDeviceToHost, s));
@@ -452,6 +456,16 @@ xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_byte
 }
 
 int64_t xgr_beam_launch_count(const xgr_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+xgr_status xgr_beam_outputs(const xgr_ctx* ctx, const int32_t** tokens, const int64_t** item_rank,
+                            const float** score, const int32_t** n_live) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "outputs: ctx is NULL");
+  if (tokens) *tokens = ctx->out_tokens;
+  if (item_rank) *item_rank = ctx->out_rank;
+  if (score) *score = ctx->out_score;
+  if (n_live) *n_live = ctx->out_nlive;
+  return XGR_OK;
+}
 
 xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t cap, int32_t* n) {
   if (!ctx || !n || (cap > 0 && !ms)) return fail(XGR_ERR_INVALID_ARG, "kernel_times: NULL argument");

@@ -63,6 +63,14 @@ struct StepArgs {
   int32_t* nlive_out;
   int32_t* parent_out;  // history of step t [batch][BW]
   int32_t* token_out;
+  // last step only (t == nd): finalize fused into the commit (item tuples, ranks, scores)
+  int32_t* fin_tokens;           // [batch][BW][nd]
+  int64_t* fin_rank;             // [batch][BW]
+  float* fin_score;              // [batch][BW]
+  int32_t* fin_nlive;            // [batch]
+  const int32_t* const* phist;   // per level: parent history [maxB][BW]
+  const int32_t* const* thist;   // per level: token history
+  int32_t nd;
   // scratch (per request), reset before each dense step
   uint32_t* theta;      // orderable(theta), 0 = no bound (-inf)
   uint32_t* surv_count;

@@ -384,16 +384,27 @@ __device__ int block_topk_fast(const uint64_t* keys, int n, int k, uint64_t* can
   uint64_t tau = sc.wsel[0];
 #pragma unroll
   for (int w = 1; w < NW; ++w) tau = sc.wsel[w] < tau ? sc.wsel[w] : tau;
-  for (int i = tid; i < n; i += T) {
-    const uint64_t v = keys[i];
-    if (v >= tau) {
-      const unsigned msk = __activemask();
-      const int leader = __ffs(msk) - 1;
-      uint32_t b = 0;
-      if (lane == leader) b = atomicAdd(&sc.n_c, (uint32_t)__popc(msk));
-      b = __shfl_sync(msk, b, leader);
-      const uint32_t p = b + __popc(msk & ((1u << lane) - 1u));
-      if (p < (uint32_t)cand_cap) cand[p] = v;
+  {
+    // count, warp scan, one shared atomic per warp, then the stores
+    uint32_t cnt = 0;
+    for (int i = tid; i < n; i += T) cnt += keys[i] >= tau;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t wb = 0;
+    if (lane == 31 && incl) wb = atomicAdd(&sc.n_c, incl);
+    uint32_t p = __shfl_sync(0xffffffffu, wb, 31) + incl - cnt;
+    if (cnt) {
+      for (int i = tid; i < n; i += T) {
+        const uint64_t v = keys[i];
+        if (v >= tau) {
+          if (p < (uint32_t)cand_cap) cand[p] = v;
+          ++p;
+        }
+      }
     }
   }
   __syncthreads();
@@ -440,15 +451,35 @@ __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, c
       a.score_out[base + j] = c;
       XGR_CHECK(b < (uint32_t)a.BW && v < (uint32_t)V, "commit req %d j %d k %d b %u v %u key %llx", req, j, k, b, v,
                 (unsigned long long)key);
-      a.node_out[base + j] = child_of_pref(a.trie, a.level, pi.fc[b], pi.fcn[b], pi.slot[b], v);
+      const uint32_t child = child_of_pref(a.trie, a.level, pi.fc[b], pi.fcn[b], pi.slot[b], v);
+      a.node_out[base + j] = child;
+      if (a.fin_tokens) {   // fused finalize (a6): backtrack the histories into the item tuple
+        int32_t* tk = a.fin_tokens + (base + j) * a.nd;
+        tk[a.nd - 1] = (int32_t)v;
+        int sidx = (int)b;
+        for (int t = a.nd - 2; t >= 0; --t) {
+          tk[t] = a.thist[t][base + sidx];
+          sidx = a.phist[t][base + sidx];
+        }
+        a.fin_rank[base + j] = (int64_t)child;   // leaf id = item rank
+        a.fin_score[base + j] = c;
+      }
     } else {
       a.parent_out[base + j] = -1;
       a.token_out[base + j] = -1;
       a.score_out[base + j] = -INFINITY;
       a.node_out[base + j] = 0xFFFFFFFFu;
+      if (a.fin_tokens) {
+        for (int t = 0; t < a.nd; ++t) a.fin_tokens[(base + j) * a.nd + t] = -1;
+        a.fin_rank[base + j] = -1;
+        a.fin_score[base + j] = -INFINITY;
+      }
     }
   }
-  if (threadIdx.x == 0) a.nlive_out[req] = k;
+  if (threadIdx.x == 0) {
+    a.nlive_out[req] = k;
+    if (a.fin_nlive) a.fin_nlive[req] = k;
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -693,35 +724,6 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
 }
 
 // ---------------------------------------------------------------------------------------------
-// k_select: per request, top-BW of the survivors (a4) and commit (a5).
-// ---------------------------------------------------------------------------------------------
-template <int T>
-__global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
-  extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
-  uint64_t* s_cand = s_keys + a.cap;
-  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
-  __shared__ TopkScratch s_sc;
-  __shared__ ParentInfo s_pi;
-  const int req = blockIdx.x, tid = threadIdx.x;
-  const uint32_t n = a.surv_count[req];
-  if (n > (uint32_t)a.cap) {
-    if (tid == 0) {
-      a.ovf[req] = 1u;
-      atomicOr(a.flags + req, kFlagOverflow);
-      count_add(a, XGR_CNT_OVERFLOW, 1);
-    }
-    return;
-  }
-  const int k = min((int)n, a.BW);
-  const uint64_t* src = a.surv + (size_t)req * a.cap;
-  for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
-  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
-  __syncthreads();
-  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
-  commit<T>(a, req, s_out, k, s_pi);
-}
-
-// ---------------------------------------------------------------------------------------------
 // k_fallback: exact top-BW for a request whose survivors overflowed the buffer. One CTA streams
 // the request's rows once per 8-bit radix digit of the 64-bit key (at most 8 passes), restricted
 // to keys >= theta. Keys are recomputed with the same formula and the lse stored by k_main, so
@@ -757,15 +759,10 @@ __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, i
 }
 
 template <int T>
-__global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs a) {
-  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
-  __shared__ uint32_t s_hist[256];
-  __shared__ uint32_t s_m32[4];
-  __shared__ ParentInfo s_pi;
-  const int req = blockIdx.x, tid = threadIdx.x;
-  if (!a.ovf[req]) return;
+__device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uint64_t* s_out,
+                                uint32_t* s_hist, uint32_t* s_m32, const ParentInfo& s_pi) {
+  const int tid = threadIdx.x;
   const int nl = nlive_of(a, req);
-  prefetch_parents<T>(a, req, nl, s_pi);
   const float th = theta_value(a.theta[req]);
   const uint64_t klo = (uint64_t)a.theta[req] << 32;
   const int k = a.BW;  // overflow => more than cap >= BW candidates >= theta
@@ -825,13 +822,46 @@ __global__ void __launch_bounds__(T) k_fallback(const __grid_constant__ StepArgs
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_select: per request, top-BW of the survivors (a4) and commit (a5).
+// ---------------------------------------------------------------------------------------------
+template <int T>
+__global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
+  uint64_t* s_cand = s_keys + a.cap;
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
+  __shared__ TopkScratch s_sc;
+  __shared__ ParentInfo s_pi;
+  const int req = blockIdx.x, tid = threadIdx.x;
+  const uint32_t n = a.surv_count[req];
+  if (n > (uint32_t)a.cap) {
+    // the survivor buffer overflowed (weak theta, massive ties): exact multi-pass fallback
+    if (tid == 0) {
+      a.ovf[req] = 1u;
+      atomicOr(a.flags + req, kFlagOverflow);
+      count_add(a, XGR_CNT_OVERFLOW, 1);
+    }
+    prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
+    __syncthreads();
+    fallback_select<T>(a, req, s_sel, s_out, s_sc.hist, s_sc.m32, s_pi);
+    return;
+  }
+  const int k = min((int)n, a.BW);
+  const uint64_t* src = a.surv + (size_t)req * a.cap;
+  for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
+  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
+  __syncthreads();
+  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  commit<T>(a, req, s_out, k, s_pi);
+}
+
+// ---------------------------------------------------------------------------------------------
 // k_sparse: one CTA per request; every legal candidate is formed on chip (no pruning needed).
 // ROOT: the single root row, gathered by the whole block. Otherwise one THREAD per live row for
 // rows with <= 16 children (all rows' dependent load chains node -> first_child -> labels ->
 // logits run concurrently), and one warp per row for the rare larger rows.
 // ---------------------------------------------------------------------------------------------
 template <int T, bool ROOT>
-__global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a) {
+__global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
   uint64_t* s_cand = s_dynk;
   uint64_t* s_keys = s_dynk + 2 * kMaxBW;
@@ -853,12 +883,50 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
   prefetch_parents<T>(a, req, nl, s_pi);
   __syncthreads();
   if (ROOT) {
+    constexpr int RPT = 16;   // root children held in registers per thread (<= 8192 children)
     for (int b = 0; b < nl; ++b) {
       float S;
       uint32_t node;
       row_state(a, req, b, S, node);
       const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
       const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      if (fe - fc <= (uint32_t)(T * RPT)) {
+        // all loads issued up front: labels, then the logits they select
+        uint32_t vv[RPT];
+        float xv[RPT];
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const uint32_t q = fc + (uint32_t)(k * T + tid);
+          vv[k] = q < fe ? (uint32_t)lab[q] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const uint32_t q = fc + (uint32_t)(k * T + tid);
+          xv[k] = q < fe ? row[vv[k]] : -INFINITY;
+        }
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) tmax = fmaxf(tmax, xv[k]);
+        const float M = block_max<T>(tmax, s_red);
+        float z = 0.f;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k)
+          if (fc + (uint32_t)(k * T + tid) < fe) z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
+        const float Z = block_sum<T>(z, s_red2);
+        const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+        const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+        if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
+        const uint32_t base = s_count;
+#pragma unroll
+        for (int k = 0; k < RPT; ++k) {
+          const uint32_t q = fc + (uint32_t)(k * T + tid);
+          if (q < fe) s_keys[base + (q - fc)] = make_key(cand_score(S, xv[k], lse), (uint32_t)b * V + vv[k]);
+        }
+        __syncthreads();
+        if (tid == 0) s_count = base + (fe - fc);
+        __syncthreads();
+        continue;
+      }
       float tmax = -INFINITY;
       for (uint32_t k = fc + tid; k < fe; k += T) tmax = fmaxf(tmax, row[lab[k]]);
       const float M = block_max<T>(tmax, s_red);
@@ -947,36 +1015,6 @@ __global__ void __launch_bounds__(T) k_sparse(const __grid_constant__ StepArgs a
   const int k = min(n, a.BW);
   block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
   commit<T>(a, req, s_out, k, s_pi);
-}
-
-// ---------------------------------------------------------------------------------------------
-// finalize (a6): backtrack histories into tuples; leaf node id = item rank.
-// ---------------------------------------------------------------------------------------------
-__global__ void k_finalize(int BW, int nd, const int32_t* const* parent_hist,
-                           const int32_t* const* token_hist, const uint32_t* node, const float* score,
-                           const int32_t* nlive, int32_t* tokens, int64_t* item_rank, float* out_score,
-                           int32_t* out_nlive) {
-  const int req = blockIdx.x;
-  const int nl = nlive[req];
-  for (int j = threadIdx.x; j < BW; j += blockDim.x) {
-    const size_t o = (size_t)req * BW + j;
-    if (j < nl) {
-      int s = j;
-      for (int t = nd - 1; t >= 0; --t) {
-        int32_t tok = token_hist[t][(size_t)req * BW + s];
-        if (tokens) tokens[o * nd + t] = tok;
-        s = parent_hist[t][(size_t)req * BW + s];
-      }
-      if (item_rank) item_rank[o] = (int64_t)node[o];
-      if (out_score) out_score[o] = score[o];
-    } else {
-      if (tokens)
-        for (int t = 0; t < nd; ++t) tokens[o * nd + t] = -1;
-      if (item_rank) item_rank[o] = -1;
-      if (out_score) out_score[o] = -INFINITY;
-    }
-  }
-  if (threadIdx.x == 0 && out_nlive) out_nlive[req] = nl;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1137,17 +1175,7 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   else return cudaErrorNotSupported;
   if (e != cudaSuccess) return e;
   k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
-  k_fallback<512><<<a.batch, 512, 0, s>>>(a);
-  *launches += 2;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finalize(int batch, int BW, int nd, const int32_t* const* parent_hist,
-                            const int32_t* const* token_hist, const uint32_t* node, const float* score,
-                            const int32_t* nlive, int32_t* tokens, int64_t* item_rank, float* out_score,
-                            int32_t* out_nlive, cudaStream_t s) {
-  k_finalize<<<batch, min(BW, 1024) < 32 ? 32 : min(BW, 1024), 0, s>>>(
-      BW, nd, parent_hist, token_hist, node, score, nlive, tokens, item_rank, out_score, out_nlive);
+  *launches += 1;
   return cudaGetLastError();
 }
 

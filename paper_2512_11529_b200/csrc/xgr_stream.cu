@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
     }
   }
   mbar_wait(&bar, 0);
+  if (a.dbg & 32) return;
 
   int kind = r_kind[g];
   const float S = r_S[g];
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
     for (int i = 0; i < 32; ++i) c[i] = -INFINITY;
   }
   if (lt == 0) r_ok[g] = kind;   // this seed row is dense, live and finite
+  if (a.dbg & 64) return;
   if (a.counters_on) {
     int lc = __reduce_add_sync(0xffffffffu, r_kind[g] ? __popc(wraw) : 0);
     if (lane == 0 && lc) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
@@ -311,22 +313,34 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
       float* cvals = s_row;            // the rows are in registers now
       if (tid == 0) b_cnt[1][0] = 0;
       __syncthreads();
+      // count, warp-scan, one shared atomic per warp, then predicated stores
+      int nsel = 0;
+      if (cmaxv >= tau0) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        if (c[i] >= tau0) {
-          const unsigned msk = __activemask();
-          const int leader = __ffs(msk) - 1;
-          int base = 0;
-          if (lane == leader) base = atomicAdd(&b_cnt[1][0], __popc(msk));
-          base = __shfl_sync(msk, base, leader);
-          const int p = base + __popc(msk & ((1u << lane) - 1u));
-          if (p < 8192) cvals[p] = c[i];
+        for (int i = 0; i < 32; ++i) nsel += c[i] >= tau0;
+      }
+      int incl = nsel;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      int wbase = 0;
+      if (lane == 31 && incl) wbase = atomicAdd(&b_cnt[1][0], incl);
+      int p = __shfl_sync(0xffffffffu, wbase, 31) + incl - nsel;
+      if (nsel) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (c[i] >= tau0) {
+            if (p < 8192) cvals[p] = c[i];
+            ++p;
+          }
         }
       }
       __syncthreads();
       const int n0 = b_cnt[1][0];
       lo = tau0;
-      if (n0 <= 8192) {
+      if (n0 <= 8192 && !(a.dbg & 16)) {
         // exact BW-th largest of the compacted candidates: MSB radix select on orderable bits
         uint32_t* hist = reinterpret_cast<uint32_t*>(s_row + 8192);
         uint32_t prefix = 0u, pmask = 0u;
@@ -379,21 +393,41 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
     }
   }
   if (tid == 0) a.theta[req] = lo > -INFINITY ? f2o(lo) : 0u;
-  // emit the seed rows' candidates >= theta (lo == -inf: every legal candidate); one global
-  // atomic per warp reserves the slots
-  uint32_t mine = 0u;
+  // emit the seed rows' candidates >= theta (lo == -inf: every legal candidate). This kernel is
+  // the request's first writer this step: a block-wide scan places the keys, no global atomics.
+  int ns = 0;
   if (kind && cmaxv >= lo) {
+    if (lo > -INFINITY) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) mine |= ((((wm >> i) & 1u) && c[i] >= lo) ? 1u : 0u) << i;
+      for (int i = 0; i < 32; ++i) ns += c[i] >= lo;   // illegal c are -inf < lo
+    } else {
+      ns = __popc(wm);
+    }
   }
-  const int ns = __popc(mine);
-  if (__any_sync(0xffffffffu, ns > 0)) {
+  int incl = ns;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  __syncthreads();   // b_cnt[0] may still be read by a slow thread of an earlier reduction
+  if (lane == 31) b_cnt[0][tid >> 5] = incl;
+  __syncthreads();
+  int woff = 0, tot_all = 0;
+  for (int w = 0; w < NT / 32; ++w) {
+    const int t = b_cnt[0][w];
+    woff += w < (tid >> 5) ? t : 0;
+    tot_all += t;
+  }
+  if (tid == 0) a.surv_count[req] = (uint32_t)tot_all;
+  if (ns) {
+    uint32_t pos = (uint32_t)(woff + incl - ns);
     const uint32_t fbase = (uint32_t)g * (uint32_t)V;
     uint64_t* sbuf = a.surv + (size_t)req * a.cap;
-    uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      if ((mine >> i) & 1u) {
+      const bool take = lo > -INFINITY ? (c[i] >= lo) : (((wm >> i) & 1u) != 0u);
+      if (take) {
         const uint32_t v = 32u * lt + 4u * (((i >> 2) + lt) & 7) + (i & 3);
         if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(c[i], fbase + v);
         ++pos;

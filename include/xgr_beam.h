@@ -75,9 +75,10 @@ typedef struct {
   int32_t top_k;      /* per-beam K. 0 or >= BW: no truncation (v1 only)  */
   int32_t max_batch;  /* max requests per step call, >= 1                                 */
   int32_t device;     /* CUDA device ordinal                                             */
-  int32_t nranks;     /* codebook shards; v1: must be 1                                   */
-  int32_t rank;       /* v1: must be 0                                                    */
-  const void* nccl_id;/* reserved for the codebook shard (ncclUniqueId); NULL in v1      */
+  int32_t nranks;     /* codebook shards G >= 1 (1: no shard). G > 1: V % G == 0 and       */
+                      /*   V/G a multiple of 128, <= 8192; use the xgr_shard_* calls      */
+  int32_t rank;       /* this shard, 0 <= rank < nranks: columns [rank*V/G, (rank+1)*V/G) */
+  const void* nccl_id;/* must be NULL: the caller performs the two all-gathers            */
   int32_t survivor_cap; /* per-request survivor buffer (keys); 0 = min(32*BW, 16384)      */
   int32_t theta_rows;   /* rows 0..theta_rows-1 seed the threshold; 0 = default (8)       */
   uint32_t flags;       /* XGR_CFG_*                                                      */
@@ -178,6 +179,28 @@ xgr_status xgr_beam_counters(xgr_ctx* ctx, uint64_t* out, void* stream);
  * (every live row, whole V). Host outputs; synchronous; not for the timed path. */
 xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_bytes,
                             int64_t* legal_candidates, void* stream);
+
+/* ---- codebook shard (nranks = G > 1) ---------------------------------------------
+ * For vocabularies too large for one GPU, G ranks each hold the columns [rank*V/G, (rank+1)*V/G)
+ * of every logits row, and the full trie (mask_build with the full item list on every rank).
+ * A step runs in three phases around two all-gathers that the caller performs (NCCL through
+ * torch.distributed; a plain copy when all ranks live in one process):
+ *   1. xgr_shard_stats: per live row the local (m, Z) over this rank's legal tokens
+ *      (m = -inf, Z = 0 when the row has none). *stats: device float pairs [batch][BW][2].
+ *   2. all-gather the stats of every rank, rank-major: gstats [G][batch][BW][2].
+ *   3. xgr_shard_select: global lse per row = fixed rank-order combine of the G pairs (identical
+ *      on every rank, R20); theta-pruned local top-BW of this rank's candidates.
+ *      *recs: device uint64 keys [batch][BW] (0-padded), *rec_n: device int32 [batch].
+ *   4. all-gather both: grecs [G][batch][BW], grec_n [G][batch].
+ *   5. xgr_shard_merge: global top-BW of the union, committed identically on every rank.
+ * logits: this rank's columns only, [batch][rows][ld] with ld >= V/G; it must stay valid until
+ * xgr_shard_select has completed on the stream. xgr_beam_step returns XGR_ERR_SEQUENCE on a
+ * sharded ctx; finalize / view / history are unchanged. All calls only enqueue. */
+xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
+                           void* stream, const float** stats);
+xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, const uint64_t** recs,
+                            const int32_t** rec_n);
+xgr_status xgr_shard_merge(xgr_ctx* ctx, const uint64_t* grecs, const int32_t* grec_n, void* stream);
 
 /* Device pointers to the ctx-owned final outputs (same layouts as xgr_beam_finalize): written by
  * the last step of every batch, valid until the next batch's last step. */

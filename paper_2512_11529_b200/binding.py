@@ -31,7 +31,8 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_finaliz
            "xgr_beam_destroy", "xgr_last_error", "xgr_abi_version", "xgr_beam_view",
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
-           "xgr_beam_kernel_times", "xgr_beam_outputs"]
+           "xgr_beam_kernel_times", "xgr_beam_outputs", "xgr_shard_stats", "xgr_shard_select",
+           "xgr_shard_merge"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -72,6 +73,9 @@ def _load():
         "xgr_beam_account": [VP, VP, VP, VP, VP],
         "xgr_beam_kernel_times": [VP, VP, VP, I32, VP],
         "xgr_beam_outputs": [VP, P(VP), P(VP), P(VP), P(VP)],
+        "xgr_shard_stats": [VP, I32, VP, I32, I64, VP, P(VP)],
+        "xgr_shard_select": [VP, VP, VP, P(VP), P(VP)],
+        "xgr_shard_merge": [VP, VP, VP, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -165,13 +169,15 @@ class BeamSearch:
     """
 
     def __init__(self, vocab: int, nd: int, beam_width: int, max_batch: int, device: int = 0,
-                 flags: int = 0, survivor_cap: int = 0, theta_rows: int = 0, top_k: int = 0):
+                 flags: int = 0, survivor_cap: int = 0, theta_rows: int = 0, top_k: int = 0,
+                 nranks: int = 1, rank: int = 0):
         import torch
         self.vocab, self.nd, self.bw, self.max_batch = vocab, nd, beam_width, max_batch
         self.device = torch.device("cuda", device)
         cfg = XgrConfig()
         cfg.vocab, cfg.nd, cfg.beam_width, cfg.top_k = vocab, nd, beam_width, top_k
-        cfg.max_batch, cfg.device, cfg.nranks, cfg.rank = max_batch, device, 1, 0
+        cfg.max_batch, cfg.device, cfg.nranks, cfg.rank = max_batch, device, nranks, rank
+        self.nranks, self.rank = nranks, rank
         cfg.survivor_cap, cfg.theta_rows, cfg.flags = survivor_cap, theta_rows, flags
         self.ctx = xgr_beam_init(cfg)
         self.batch = None
@@ -226,6 +232,35 @@ class BeamSearch:
                       self._stream(stream))
         self.batch = b
         self.t += 1
+
+    # ---- codebook shard phases (nranks > 1): the caller all-gathers between them ----------------
+    def shard_stats(self, logits, stream=None):
+        """logits: this rank's columns, CUDA fp32 [batch][rows][ld]. Returns a [batch][BW][2]
+        fp32 view of the local (m, Z) per row (valid until the next shard call)."""
+        import torch
+        b, rows = logits.shape[0], logits.shape[1]
+        p = ctypes.c_void_p()
+        _check(lib.xgr_shard_stats(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), rows,
+                                   logits.stride(1), self._stream(stream), ctypes.byref(p)))
+        self.batch = b
+        self._shard_logits = logits   # must stay alive until shard_select completes
+        return _view(p.value, (b, self.bw, 2), "<f4", self.device)
+
+    def shard_select(self, gstats, stream=None):
+        """gstats: CUDA fp32 [nranks][batch][BW][2] (all ranks' stats, rank-major). Returns
+        (recs uint64-as-int64 [batch][BW], rec_n int32 [batch]) views."""
+        r, n = ctypes.c_void_p(), ctypes.c_void_p()
+        _check(lib.xgr_shard_select(self.ctx, ctypes.c_void_p(gstats.data_ptr()), self._stream(stream),
+                                    ctypes.byref(r), ctypes.byref(n)))
+        return (_view(r.value, (self.batch, self.bw), "<i8", self.device),
+                _view(n.value, (self.batch,), "<i4", self.device))
+
+    def shard_merge(self, grecs, grec_n, stream=None):
+        """grecs int64 [nranks][batch][BW], grec_n int32 [nranks][batch] (all ranks, rank-major)."""
+        _check(lib.xgr_shard_merge(self.ctx, ctypes.c_void_p(grecs.data_ptr()),
+                                   ctypes.c_void_p(grec_n.data_ptr()), self._stream(stream)))
+        self.t += 1
+        self._shard_logits = None
 
     def finalize_in_place(self, stream=None):
         """Ends the batch without copying: results stay in the ctx buffers (outputs_view())."""
@@ -326,3 +361,35 @@ class BeamSearch:
         _check(lib.xgr_beam_account(self.ctx, ctypes.byref(a), ctypes.byref(f), ctypes.byref(lg),
                                     self._stream()))
         return {"alg_bytes": a.value, "full_bytes": f.value, "legal": lg.value}
+
+
+class ShardedBeamSearch:
+    """One rank of a codebook-sharded beam search: wraps a BeamSearch with
+    nranks > 1 and performs the two all-gathers between the shard phases.
+
+    all_gather(t) -> tensor [nranks, *t.shape] in rank order. By default it is
+    torch.distributed.all_gather_into_tensor on the given process group (NCCL over NVLink on a
+    multi-GPU node); a single-process emulator passes its own concatenation."""
+
+    def __init__(self, bs: "BeamSearch", group=None, all_gather=None):
+        self.bs = bs
+        self.group = group
+        self._ag = all_gather or self._dist_all_gather
+
+    def _dist_all_gather(self, t):
+        import torch
+        import torch.distributed as dist
+        out = torch.empty((self.bs.nranks, *t.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
+        return out
+
+    def step(self, logits_local, stream=None):
+        stats = self.bs.shard_stats(logits_local, stream)
+        gstats = self._ag(stats)
+        recs, n = self.bs.shard_select(gstats, stream)
+        grecs = self._ag(recs)
+        gn = self._ag(n)
+        self.bs.shard_merge(grecs, gn, stream)
+
+    def finalize(self, **kw):
+        return self.bs.finalize(**kw)

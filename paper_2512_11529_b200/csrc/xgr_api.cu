@@ -17,6 +17,10 @@ namespace xgr {
 cudaError_t configure_kernels(int cap);
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
+cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s);
+cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches);
+cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
+                               cudaStream_t s);
 cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
                             int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s);
 cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched,
@@ -52,6 +56,13 @@ struct xgr_ctx {
   StepArgs last{};
   int last_rows = 0;
   int64_t launches = 0;             // kernels launched by this ctx (host-side count)
+  // codebook shard (nranks > 1)
+  float2* shard_stats = nullptr;    // [maxB][BW] this rank's (m, Z)
+  uint64_t* shard_rec = nullptr;    // [maxB][BW] this rank's local top-BW keys
+  int32_t* shard_rec_n = nullptr;   // [maxB]
+  StepArgs shard_args{};
+  int shard_rows = 0;
+  int shard_phase = 0;              // 0: expect stats, 1: expect select, 2: expect merge
   // XGR_CFG_TIMING: ring of event pairs around the dense-route streaming kernel
   std::vector<cudaEvent_t> ev;      // 2 * kTimingRing
   std::vector<int32_t> ev_step;
@@ -101,6 +112,9 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->out_rank);
   cudaFree(c->out_score);
   cudaFree(c->out_nlive);
+  cudaFree(c->shard_stats);
+  cudaFree(c->shard_rec);
+  cudaFree(c->shard_rec_n);
 }
 
 extern "C" {
@@ -124,8 +138,16 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.top_k > 0 && c.top_k < c.beam_width)
     return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width is not implemented (v1)");
   if (c.max_batch < 1) return fail(XGR_ERR_INVALID_ARG, "init: max_batch < 1");
-  if (c.nranks != 1 || c.rank != 0 || c.nccl_id)
-    return fail(XGR_ERR_UNSUPPORTED, "init: codebook sharding (nranks > 1) is not implemented (v1)");
+  if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks)
+    return fail(XGR_ERR_INVALID_ARG, "init: need 0 <= rank < nranks");
+  if (c.nccl_id) return fail(XGR_ERR_UNSUPPORTED, "init: nccl_id must be NULL (the caller performs the all-gathers)");
+  if (c.nranks > 1) {
+    if (c.vocab % c.nranks != 0) return fail(XGR_ERR_INVALID_ARG, "init: vocab %% nranks != 0");
+    const int vl = c.vocab / c.nranks;
+    if (vl % 128 != 0 || vl > 8192)
+      return fail(XGR_ERR_UNSUPPORTED, "init: codebook shard needs V/nranks a multiple of 128 and <= 8192");
+    if (c.nranks > 64) return fail(XGR_ERR_UNSUPPORTED, "init: nranks > 64");
+  }
   if (c.survivor_cap < 0 || c.theta_rows < 0) return fail(XGR_ERR_INVALID_ARG, "init: negative knob");
   for (int i = 0; i < 5; ++i)
     if (c.reserved[i]) return fail(XGR_ERR_INVALID_ARG, "init: reserved fields must be zero");
@@ -170,6 +192,11 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->out_rank, nb * 8);
   if (e == cudaSuccess) e = al((void**)&x->out_score, nb * 4);
   if (e == cudaSuccess) e = al((void**)&x->out_nlive, (size_t)x->maxB * 4);
+  if (e == cudaSuccess && c.nranks > 1) {
+    e = al((void**)&x->shard_stats, nb * sizeof(float2));
+    if (e == cudaSuccess) e = al((void**)&x->shard_rec, nb * 8);
+    if (e == cudaSuccess) e = al((void**)&x->shard_rec_n, (size_t)x->maxB * 4);
+  }
   if (e == cudaSuccess) {
     std::vector<int32_t*> ph(x->nd), th(x->nd);
     for (int t = 0; t < x->nd; ++t) {
@@ -216,24 +243,26 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
   return XGR_OK;
 }
 
-xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
-                         void* stream) {
-  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "step: ctx is NULL");
-  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "step: mask_build has not run");
-  if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "step: already %d steps; call finalize", ctx->nd);
-  if (!logits) return fail(XGR_ERR_INVALID_ARG, "step: logits is NULL");
-  if (batch < 1 || batch > ctx->maxB) return fail(XGR_ERR_INVALID_ARG, "step: batch %d not in 1..%d", batch, ctx->maxB);
+// Validates a step's inputs and fills the launch arguments (shared by xgr_beam_step and the
+// codebook-shard phases). `what` names the caller in error messages.
+static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
+                            const char* what, StepArgs& a, int& rows_live) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "%s: ctx is NULL", what);
+  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "%s: mask_build has not run", what);
+  if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "%s: already %d steps; call finalize", what, ctx->nd);
+  if (!logits) return fail(XGR_ERR_INVALID_ARG, "%s: logits is NULL", what);
+  if (batch < 1 || batch > ctx->maxB)
+    return fail(XGR_ERR_INVALID_ARG, "%s: batch %d not in 1..%d", what, batch, ctx->maxB);
   if (ctx->step > 0 && batch != ctx->batch)
-    return fail(XGR_ERR_INVALID_ARG, "step: batch %d differs from this batch's %d", batch, ctx->batch);
+    return fail(XGR_ERR_INVALID_ARG, "%s: batch %d differs from this batch's %d", what, batch, ctx->batch);
   const int t = ctx->step + 1;
   const int need_rows = (t == 1) ? 1 : ctx->BW;
-  if (rows < need_rows) return fail(XGR_ERR_INVALID_ARG, "step %d: rows %d < %d", t, rows, need_rows);
-  if (ld < ctx->V) return fail(XGR_ERR_INVALID_ARG, "step: ld %lld < V %d", (long long)ld, ctx->V);
+  if (rows < need_rows) return fail(XGR_ERR_INVALID_ARG, "%s (step %d): rows %d < %d", what, t, rows, need_rows);
+  const int Vl = ctx->V / ctx->cfg.nranks;
+  if (ld < Vl) return fail(XGR_ERR_INVALID_ARG, "%s: ld %lld < %d columns", what, (long long)ld, Vl);
   if ((reinterpret_cast<uintptr_t>(logits) & 15u) || (ld & 3))
-    return fail(XGR_ERR_ALIGNMENT, "step: logits must be 16-byte aligned and ld %% 4 == 0");
-  cudaStream_t s = (cudaStream_t)stream;
+    return fail(XGR_ERR_ALIGNMENT, "%s: logits must be 16-byte aligned and ld %% 4 == 0", what);
 
-  StepArgs a;
   memset(&a, 0, sizeof(a));
   a.trie = trie_dev(ctx->trie);
   a.logits = logits;
@@ -247,6 +276,9 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
   a.theta_rows = ctx->R0;
   a.counters_on = (ctx->cfg.flags & XGR_CFG_COUNTERS) ? 1 : 0;
   a.no_prune = (ctx->cfg.flags & XGR_CFG_NO_PRUNE) ? 1 : 0;
+  a.col0 = ctx->cfg.rank * Vl;
+  a.Vl = Vl;
+  a.nranks = ctx->cfg.nranks;
   const int in = (t - 1) & 1, outi = t & 1;
   if (t > 1) {
     a.score_in = ctx->score[in];
@@ -275,14 +307,28 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
     a.fin_score = ctx->out_score;
     a.fin_nlive = ctx->out_nlive;
   }
+  static const int dbg_flags = getenv("XGR_DEBUG_FLAGS") ? atoi(getenv("XGR_DEBUG_FLAGS")) : 0;
+  a.dbg = dbg_flags;
+  rows_live = need_rows;   // upper bound on the live rows of any request this step
+  return XGR_OK;
+}
 
-  const int rows_live = need_rows;  // upper bound on live rows of any request this step
+xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
+                         void* stream) {
+  StepArgs a;
+  int rows_live = 0;
+  xgr_status st = step_args(ctx, batch, logits, rows, ld, "step", a, rows_live);
+  if (st != XGR_OK) return st;
+  if (ctx->cfg.nranks > 1)
+    return fail(XGR_ERR_SEQUENCE, "step: codebook-sharded ctx: use xgr_shard_stats/select/merge");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int t = a.t;
   const int64_t maxc = ctx->trie.lv[t - 1].max_children;
   const int64_t sparse_keys = (int64_t)rows_live * maxc;
   const bool sparse_route =
       !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sparse_keys <= kSparseCap;
   if (!sparse_route && ctx->V > 16384)
-    return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 is not implemented yet");
+    return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 needs the codebook shard (nranks > 1)");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (!ctx->ev.empty() && !sparse_route && ctx->ev_head - ctx->ev_tail < kTimingRing) {
@@ -294,14 +340,71 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
   }
   int launches = 0;
   a.sparse_cap = (int)sparse_keys;
-  static const int dbg_flags = getenv("XGR_DEBUG_FLAGS") ? atoi(getenv("XGR_DEBUG_FLAGS")) : 0;
-  a.dbg = dbg_flags;
   ACK(launch_step(a, rows_live, sparse_route, (int)sparse_keys, s, ev0, ev1, &launches));
   ctx->launches += launches;
   ctx->batch = batch;
   ctx->step = t;
   ctx->last = a;
   ctx->last_rows = rows_live;
+  return XGR_OK;
+}
+
+// ---- codebook shard: stats -> (all-gather) -> select -> (all-gather) -> merge -------------------
+xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
+                           void* stream, const float** stats) {
+  StepArgs a;
+  int rows_live = 0;
+  xgr_status st = step_args(ctx, batch, logits, rows, ld, "shard_stats", a, rows_live);
+  if (st != XGR_OK) return st;
+  if (ctx->shard_phase != 0) return fail(XGR_ERR_SEQUENCE, "shard_stats: previous step not merged");
+  if (!stats) return fail(XGR_ERR_INVALID_ARG, "shard_stats: stats is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (a.t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
+  a.stats_out = ctx->shard_stats;
+  ACK(launch_shard_stats(a, rows_live, s));
+  ctx->launches += 1;
+  ctx->batch = batch;
+  ctx->shard_args = a;
+  ctx->shard_rows = rows_live;
+  ctx->shard_phase = 1;
+  *stats = reinterpret_cast<const float*>(ctx->shard_stats);
+  return XGR_OK;
+}
+
+xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, const uint64_t** recs,
+                            const int32_t** rec_n) {
+  if (!ctx || !gstats || !recs || !rec_n) return fail(XGR_ERR_INVALID_ARG, "shard_select: NULL argument");
+  if (ctx->shard_phase != 1) return fail(XGR_ERR_SEQUENCE, "shard_select: call shard_stats first");
+  StepArgs a = ctx->shard_args;
+  a.stats_out = nullptr;
+  a.gstats = reinterpret_cast<const float2*>(gstats);
+  a.rec_out = ctx->shard_rec;
+  a.rec_n = ctx->shard_rec_n;
+  cudaStream_t s = (cudaStream_t)stream;
+  int launches = 0;
+  ACK(launch_shard_select(a, ctx->shard_rows, s, &launches));
+  ctx->launches += launches;
+  ctx->shard_phase = 2;
+  *recs = ctx->shard_rec;
+  *rec_n = ctx->shard_rec_n;
+  return XGR_OK;
+}
+
+xgr_status xgr_shard_merge(xgr_ctx* ctx, const uint64_t* grecs, const int32_t* grec_n, void* stream) {
+  if (!ctx || !grecs || !grec_n) return fail(XGR_ERR_INVALID_ARG, "shard_merge: NULL argument");
+  if (ctx->shard_phase != 2) return fail(XGR_ERR_SEQUENCE, "shard_merge: call shard_select first");
+  StepArgs a = ctx->shard_args;
+  a.stats_out = nullptr;
+  a.gstats = nullptr;
+  a.rec_out = nullptr;
+  a.rec_n = nullptr;
+  cudaStream_t s = (cudaStream_t)stream;
+  ACK(launch_shard_merge(a, grecs, grec_n, s));
+  ctx->launches += 1;
+  ctx->step = a.t;
+  ctx->last = a;
+  ctx->last_rows = ctx->shard_rows;
+  ctx->shard_phase = 0;
   return XGR_OK;
 }
 

@@ -79,7 +79,37 @@ struct StepArgs {
   float* lse;           // [batch][BW] per-row lse (NaN: row not read)
   uint32_t* flags;      // sticky per-request status bits
   unsigned long long* counters;
+  // codebook shard (nranks > 1): this rank's logits hold columns [col0, col0 + Vl) of V
+  int32_t col0;
+  int32_t Vl;
+  int32_t nranks;
+  float2* stats_out;            // stats phase: [batch][BW] local (m, Z) of each live row
+  const float2* gstats;         // select phase: [nranks][batch][BW] all ranks' (m, Z)
+  uint64_t* rec_out;            // select phase: [batch][BW] local top-BW keys (0-padded)
+  int32_t* rec_n;               // select phase: [batch] number of local records
 };
+
+// Global lse of row b from all ranks' (m, Z) in ascending rank order (R20):
+// M = max_g m_g, Z = sum_g Z_g * 2^((m_g - M) * log2 e), lse = M + max(ln Z, 0).
+__device__ __forceinline__ float shard_lse(const StepArgs& a, int req, int b, bool& finite) {
+  const size_t stride = (size_t)a.batch * a.BW;
+  const size_t o = (size_t)req * a.BW + b;
+  float M = -INFINITY;
+  for (int g = 0; g < a.nranks; ++g) M = fmaxf(M, a.gstats[g * stride + o].x);
+  float Z = 0.f;
+  for (int g = 0; g < a.nranks; ++g) {
+    const float2 p = a.gstats[g * stride + o];
+    if (p.y > 0.f) {
+      float e;
+      asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(__fmul_rn(__fsub_rn(p.x, M), 1.4426950408889634f)));
+      Z = __fadd_rn(Z, __fmul_rn(p.y, e));
+    } else if (p.y != p.y) {
+      Z = p.y;   // a rank saw a non-finite legal logit
+    }
+  }
+  finite = (Z > 0.5f) && (Z <= 3.0e38f) && (M > -INFINITY);
+  return __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+}
 
 constexpr uint32_t kFlagNonfinite = 1u;
 constexpr uint32_t kFlagOverflow = 2u;

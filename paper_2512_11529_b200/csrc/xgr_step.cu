@@ -242,7 +242,7 @@ __device__ __forceinline__ uint64_t warp_sort_desc_u64(uint64_t v) {
 // 32 in registers (shuffle bitonic) and writes it back in place; a key's final rank is its index
 // in its own list plus, for every other list, the number of greater keys (binary search).
 template <int T>
-__device__ void sort_desc_to(uint64_t* sel, int k, uint64_t* out) {
+__device__ void sort_desc_to(uint64_t* sel, int k, uint64_t* out, int k_out = 1 << 30) {
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int nl = (k + 31) >> 5;
   for (int w = warp; w < nl; w += T / 32) {
@@ -271,7 +271,7 @@ __device__ void sort_desc_to(uint64_t* sel, int k, uint64_t* out) {
       r += lo;
     }
     XGR_CHECK(r < k, "sort_desc_to r %d k %d", r, k);
-    out[r] = v;
+    if (r < k_out) out[r] = v;
   }
   __syncthreads();
 }
@@ -361,7 +361,7 @@ struct TopkScratch {
 };
 
 template <int T>
-__device__ int block_topk_fast(const uint64_t* keys, int n, int k, uint64_t* cand, int cand_cap,
+__device__ int block_topk_fast(uint64_t* keys, int n, int k, uint64_t* cand, int cand_cap,
                                uint64_t* sel, uint64_t* out, TopkScratch& sc) {
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   constexpr int NW = T / 32;
@@ -439,6 +439,11 @@ template <int T>
 __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, const ParentInfo& pi) {
   const int V = a.trie.V;
   const size_t base = (size_t)req * a.BW;
+  if (a.rec_out) {   // codebook-shard select phase: this rank's local top-BW keys, no state update
+    for (int j = threadIdx.x; j < a.BW; j += T) a.rec_out[base + j] = j < k ? sel[j] : 0ull;
+    if (threadIdx.x == 0) a.rec_n[req] = k;
+    return;
+  }
   for (int j = threadIdx.x; j < a.BW; j += T) {
     if (j < k) {
       uint64_t key = sel[j];
@@ -732,28 +737,30 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
 template <int T, typename F>
 __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, int b, float S,
                                                    float lse, uint32_t node, F&& f) {
+  // this rank's columns [col0, col0 + Vl) (the whole row unless codebook-sharded)
   const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
   if (slot >= 0) {
-    const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W;
-    const int V = a.trie.V;
-    for (int q = threadIdx.x; 4 * q < V; q += T) {
+    const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W + (a.col0 >> 5);
+    const int Vl = a.Vl;
+    for (int q = threadIdx.x; 4 * q < Vl; q += T) {
       uint32_t nb = (bm[q >> 3] >> ((q & 7) * 4)) & 0xFu;
       if (!nb) continue;
       float4 x = ld_stream4(row + 4 * q);
       float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if ((nb >> j) & 1u) f(make_key(cand_score(S, xs[j], lse), fbase + 4u * q + j));
+        if ((nb >> j) & 1u) f(make_key(cand_score(S, xs[j], lse), fbase + (uint32_t)a.col0 + 4u * q + j));
     }
   } else {
     const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
     const uint16_t* lab = a.trie.lv[a.level + 1].label;
     for (uint32_t k = fc + threadIdx.x; k < fe; k += T) {
       uint32_t v = lab[k];
-      f(make_key(cand_score(S, row[v], lse), fbase + v));
+      if (v < (uint32_t)a.col0 || v >= (uint32_t)(a.col0 + a.Vl)) continue;
+      f(make_key(cand_score(S, row[v - a.col0], lse), fbase + v));
     }
   }
 }
@@ -850,7 +857,47 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
   prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
   __syncthreads();
+  if (a.dbg & 128) return;
   block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  if (a.dbg & 256) return;
+  commit<T>(a, req, s_out, k, s_pi);
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_merge (codebook shard): every rank's local top-BW keys of a request, all-gathered
+// into [nranks][batch][BW]; the global top-BW of their union is the step's result (each key
+// carries its global score and flat index), committed identically on every rank (each rank holds
+// the whole trie, so child ids are computed locally).
+// ---------------------------------------------------------------------------------------------
+template <int T>
+__global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a, const uint64_t* grec,
+                                             const int32_t* grec_n) {
+  extern __shared__ __align__(16) uint64_t s_keys[];  // [nranks * BW] keys, then [2 * kMaxBW]
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
+  __shared__ TopkScratch s_sc;
+  __shared__ ParentInfo s_pi;
+  __shared__ int s_off[65];
+  const int req = blockIdx.x, tid = threadIdx.x;
+  uint64_t* s_cand = s_keys + (size_t)a.nranks * a.BW;
+  if (tid == 0) {
+    int o = 0;
+    for (int g = 0; g < a.nranks; ++g) {
+      s_off[g] = o;
+      o += grec_n[g * a.batch + req];
+    }
+    s_off[a.nranks] = o;
+  }
+  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
+  __syncthreads();
+  const int n = s_off[a.nranks];
+  for (int g = 0; g < a.nranks; ++g) {
+    const int ng = s_off[g + 1] - s_off[g];
+    const uint64_t* src = grec + ((size_t)g * a.batch + req) * a.BW;
+    for (int i = tid; i < ng; i += T) s_keys[s_off[g] + i] = src[i];
+  }
+  __syncthreads();
+  const int k = min(n, a.BW);
+  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
   commit<T>(a, req, s_out, k, s_pi);
 }
 
@@ -1176,6 +1223,29 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   if (e != cudaSuccess) return e;
   k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
   *launches += 1;
+  return cudaGetLastError();
+}
+
+bool stream_supported(int V);
+cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s);
+cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s);
+
+// Codebook shard, select phase: theta seed + emission with the global lse, then this rank's
+// local top-BW records (k_select writes records instead of committing when a.rec_out is set).
+cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches) {
+  cudaError_t e = launch_shard_emit(a, rows, s);
+  if (e != cudaSuccess) return e;
+  k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
+                               cudaStream_t s) {
+  const size_t smem = ((size_t)a.nranks * a.BW + 2 * kMaxBW) * sizeof(uint64_t);
+  cudaError_t e = cudaFuncSetAttribute(k_merge<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_merge<512><<<a.batch, 512, smem, s>>>(a, grec, grec_n);
   return cudaGetLastError();
 }
 

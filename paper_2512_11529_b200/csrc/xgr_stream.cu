@@ -95,7 +95,12 @@ struct Desc {
   int32_t req, b, kind, slot;  // kind: 0 nothing to do, 1 dense row in stage, 2 sparse row
   float S;
   uint32_t node;
+  float lse;                   // shard-emit mode: the row's global lse (from all ranks' stats)
 };
+
+// k_stream modes: normal step; codebook-shard stats pass (local (m, Z) per row, no emission);
+// codebook-shard emit pass (global lse given, no (m, Z) work).
+constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2;
 
 // Consumer-group reductions: warp butterfly, then every consumer thread folds the per-warp
 // partials in a fixed order (bitwise-identical, deterministic results in every thread).
@@ -135,7 +140,7 @@ __device__ __forceinline__ int cisum(int v, int* part) {
 // ------------------------------------------------------------------------------------------
 // k_seed
 // ------------------------------------------------------------------------------------------
-template <int CTR, int R0>
+template <int CTR, int R0, int MODE = kModeNormal>
 __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ StepArgs a) {
   constexpr int NT = CTR * R0;
   extern __shared__ __align__(128) float s_dyn[];
@@ -143,7 +148,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
   uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dyn + R0 * 32 * CTR);  // [R0][CTR]
   __shared__ __align__(8) uint64_t bar;
   __shared__ int r_kind[R0], r_slot[R0], r_ok[R0];
-  __shared__ float r_S[R0];
+  __shared__ float r_S[R0], r_lse[R0];
   __shared__ float g_max[NT / 32], g_sum[NT / 32];
   __shared__ float b_red[2][NT / 32];
   __shared__ int b_cnt[2][NT / 32];
@@ -161,6 +166,14 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
       row_state(a, req, tid, S, node);
       slot = L.dense_slot ? L.dense_slot[node] : -1;
       kind = slot >= 0 ? 1 : 0;   // sparse seed rows are left to k_stream
+      if (MODE == kModeShardEmit && kind) {
+        bool fin;
+        r_lse[tid] = shard_lse(a, req, tid, fin);
+        if (!fin) {
+          r_lse[tid] = __int_as_float(0x7fc00000);
+          atomicOr(a.flags + req, kFlagNonfinite);
+        }
+      }
     }
     r_kind[tid] = kind;
     r_slot[tid] = slot;
@@ -176,15 +189,16 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
   __syncthreads();
   if (tid == 0) {
     uint32_t bytes = 0;
-    for (int r = 0; r < R0; ++r) bytes += r_kind[r] ? (uint32_t)(V + W) * 4u : 0u;
+    const uint32_t rb = (uint32_t)a.Vl * 4u, mb = (uint32_t)(a.Vl >> 5) * 4u;
+    for (int r = 0; r < R0; ++r) bytes += r_kind[r] ? rb + mb : 0u;
     if (bytes) {
       mbar_arrive_tx(&bar, bytes);
       const uint64_t pol = policy_evict_first();
       for (int r = 0; r < R0; ++r) {
         if (!r_kind[r]) continue;
         const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
-        bulk_g2s(s_row + (size_t)r * 32 * CTR, row, (uint32_t)V * 4u, &bar, pol);
-        bulk_g2s(s_msk + (size_t)r * CTR, L.bitmap + (size_t)r_slot[r] * W, (uint32_t)W * 4u, &bar, pol);
+        bulk_g2s(s_row + (size_t)r * 32 * CTR, row, rb, &bar, pol);
+        bulk_g2s(s_msk + (size_t)r * CTR, L.bitmap + (size_t)r_slot[r] * W + (a.col0 >> 5), mb, &bar, pol);
       }
     } else {
       mbar_arrive(&bar);
@@ -213,6 +227,12 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
       c[4 * i + 3] = (wm >> (4 * i + 3)) & 1u ? x.w : -INFINITY;
       tmax = fmaxf(tmax, fmaxf(fmaxf(c[4 * i], c[4 * i + 1]), fmaxf(c[4 * i + 2], c[4 * i + 3])));
     }
+    float lse;
+    bool finite;
+    if (MODE == kModeShardEmit) {
+      lse = r_lse[g];
+      finite = lse == lse;
+    } else {
     // group (= row) reductions on named barrier 1 + g
     float v = wmax(tmax);
     if (lane == 0) g_max[tid >> 5] = v;
@@ -233,8 +253,9 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
     float Z = g_sum[g * (CTR / 32)];
 #pragma unroll
     for (int i = 1; i < CTR / 32; ++i) Z += g_sum[g * (CTR / 32) + i];
-    const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-    const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    finite = (Z > 0.5f) && (Z <= 3.0e38f);
+    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    }   // MODE != kModeShardEmit
     if (lt == 0) {
       a.lse[(size_t)req * BW + g] = finite ? lse : __int_as_float(0x7fc00000);
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
@@ -422,7 +443,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
   if (tid == 0) a.surv_count[req] = (uint32_t)tot_all;
   if (ns) {
     uint32_t pos = (uint32_t)(woff + incl - ns);
-    const uint32_t fbase = (uint32_t)g * (uint32_t)V;
+    const uint32_t fbase = (uint32_t)g * (uint32_t)V + (uint32_t)a.col0;
     uint64_t* sbuf = a.surv + (size_t)req * a.cap;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
@@ -456,7 +477,7 @@ __device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
   }
 }
 
-template <int EPT, int G, int NS, int MINB = 1>
+template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal>
 __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   constexpr int GT = 256;          // consumer threads per group
@@ -501,6 +522,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       float S, th;
       uint32_t node;
       int slot;
+      float lse;
     };
     auto fetch_raw = [&](int k0) {
       Meta m;
@@ -512,6 +534,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       m.th = -INFINITY;
       m.node = 0;
       m.slot = -1;
+      m.lse = 0.f;
       if (w < total) {
         m.b = w / a.batch;
         m.req = w - m.b * a.batch;
@@ -519,7 +542,15 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         m.live = m.b < nl;
         if (m.live) {
           row_state(a, m.req, m.b, m.S, m.node);
-          m.th = theta_value(a.theta[m.req]);
+          if (MODE != kModeStats) m.th = theta_value(a.theta[m.req]);
+          if (MODE == kModeShardEmit) {
+            bool fin;
+            m.lse = shard_lse(a, m.req, m.b, fin);
+            if (!fin) {
+              m.lse = __int_as_float(0x7fc00000);
+              atomicOr(a.flags + m.req, kFlagNonfinite);
+            }
+          }
         }
       }
       return m;
@@ -536,7 +567,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       fetch_slot(m1);
       // decisions for the current batch (its loads completed during the previous batch)
       int kind = 0;
-      if (m0.live) {
+      if (m0.live && !(MODE == kModeShardEmit && m0.lse != m0.lse)) {
         if (m0.S < m0.th) {   // every candidate of the row is <= S_b < theta: skip unread
           a.lse[(size_t)m0.req * BW + m0.b] = __int_as_float(0x7fc00000);
           if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
@@ -554,6 +585,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         const float jS = __shfl_sync(0xffffffffu, m0.S, j);
         const float jth = __shfl_sync(0xffffffffu, m0.th, j);
         const uint32_t jnode = __shfl_sync(0xffffffffu, m0.node, j);
+        const float jlse = __shfl_sync(0xffffffffu, m0.lse, j);
         if (lane == 0) {
           const int st = kj % NS;
           if (kj >= NS) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
@@ -564,14 +596,15 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
           d.slot = jslot;
           d.S = jS;
           d.node = jnode;
+          d.lse = jlse;
           desc[st] = d;
           s_th[st] = jth;
           if (jkind == 1) {
             const float* row = a.logits + (size_t)jreq * a.req_stride + (size_t)jb * a.ld;
-            const uint32_t rb = (uint32_t)V * 4u, mb = (uint32_t)W * 4u;
+            const uint32_t rb = (uint32_t)a.Vl * 4u, mb = (uint32_t)(a.Vl >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
             bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
-            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W, mb, &full[st], pol);
+            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (a.col0 >> 5), mb, &full[st], pol);
           } else {
             mbar_arrive(&full[st]);
           }
@@ -642,24 +675,50 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (d.kind == 0) continue;
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
-      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
-      const uint32_t fc = L.first_child[d.node], fe = L.first_child[d.node + 1];
-      float tm = -INFINITY;
-      for (uint32_t q = fc + lt; q < fe; q += GT) tm = fmaxf(tm, row[lab[q]]);
-      const float M = gmax(tm);
-      float z = 0.f;
-      for (uint32_t q = fc + lt; q < fe; q += GT)
-        z += ex2f(__fmul_rn(__fsub_rn(row[lab[q]], M), kLog2eS));
-      const float Z = gsum(z);
-      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
-      if (lt == 0) {
-        a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
-        if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
-        if (a.counters_on) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)(fe - fc));
+      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
+      uint32_t fc = L.first_child[d.node], fe = L.first_child[d.node + 1];
+      if (a.Vl != V) {   // codebook shard: the children whose token lies in this rank's columns
+        uint32_t lo = fc, hi = fe;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (lab[mid] < (uint32_t)a.col0) lo = mid + 1; else hi = mid;
+        }
+        fc = lo;
+        hi = fe;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (lab[mid] < (uint32_t)(a.col0 + a.Vl)) lo = mid + 1; else hi = mid;
+        }
+        fe = lo;
+      }
+      float M = 0.f, lse;
+      bool finite;
+      if (MODE == kModeShardEmit) {
+        lse = d.lse;
+        finite = true;
+        if (lt == 0) a.lse[(size_t)req * BW + b] = lse;
+      } else {
+        float tm = -INFINITY;
+        for (uint32_t q = fc + lt; q < fe; q += GT) tm = fmaxf(tm, row[lab[q]]);
+        M = gmax(tm);
+        float z = 0.f;
+        for (uint32_t q = fc + lt; q < fe; q += GT)
+          z += ex2f(__fmul_rn(__fsub_rn(row[lab[q]], M), kLog2eS));
+        const float Z = gsum(z);
+        if (MODE == kModeStats) {   // local (m, Z); an empty slice is (-inf, 0)
+          if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+          continue;
+        }
+        finite = (Z > 0.5f) && (Z <= 3.0e38f);
+        lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+        if (lt == 0) {
+          a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
+          if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+          if (a.counters_on) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)(fe - fc));
+        }
       }
       if (!finite) continue;
-      if (!(cand_score(S, M, lse) >= th)) continue;
+      if (MODE == kModeNormal && !(cand_score(S, M, lse) >= th)) continue;
       const uint32_t fbase = (uint32_t)b * (uint32_t)V;
       for (uint32_t q0 = fc; q0 < fe; q0 += GT) {
         const uint32_t q = q0 + lt;
@@ -700,6 +759,11 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     float tmax = -INFINITY;
 #pragma unroll
     for (int e = 0; e < EPT; e += 4) tmax = fmaxf(tmax, fmaxf(fmaxf(x[e], x[e + 1]), fmaxf(x[e + 2], x[e + 3])));
+    float lse;
+    if (MODE == kModeShardEmit) {
+      lse = d.lse;   // global lse of the row, from all ranks' (m, Z)
+      if (lt == 0) a.lse[(size_t)req * BW + b] = lse;   // for the exact overflow fallback
+    } else {
     // warp-local (m_w, z_w), one group barrier, then combine the GT/32 pairs
     const float mw = wmax(tmax);
     const float mws = mw == -INFINITY ? 0.0f : mw;
@@ -729,8 +793,12 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
     M = __shfl_sync(0xffffffffu, M, 0);
     const float Z = __shfl_sync(0xffffffffu, zi, 0);
+    if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
+      if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+      continue;
+    }
     const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-    const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
     if (lt == 0) {
       a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
@@ -748,6 +816,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
     }
+    }   // MODE != kModeShardEmit
     // select this thread's candidates (bit e of `mine`), then one atomic per warp reserves slots
     uint64_t mine = 0ull;
     if (th > -INFINITY) {
@@ -769,18 +838,18 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
       // included, is a candidate; legality re-read from the node's bitmap in global memory
-      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (lt >> 3);
+      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (a.col0 >> 5) + (lt >> 3);
 #pragma unroll
       for (int i = 0; i < NF4; ++i) {
         const uint32_t q4 = (uint32_t)(i * GT + lt);
-        const uint32_t nb = (4 * q4 < (uint32_t)V) ? ((__ldg(gm + i * (GT / 8)) >> nsh) & 0xFu) : 0u;
+        const uint32_t nb = (4 * q4 < (uint32_t)a.Vl) ? ((__ldg(gm + i * (GT / 8)) >> nsh) & 0xFu) : 0u;
         mine |= (uint64_t)nb << (4 * i);
       }
     }
     const int ns = __popcll(mine);
     if ((a.dbg & 1) == 0 && __any_sync(0xffffffffu, ns > 0)) {
       flush();
-      const uint32_t fbase = (uint32_t)b * (uint32_t)V;
+      const uint32_t fbase = (uint32_t)b * (uint32_t)V + (uint32_t)a.col0;
       if (__any_sync(0xffffffffu, ns > 2)) {
         // many candidates in one lane (weak theta): reserve and write synchronously
         uint64_t* sbuf = a.surv + (size_t)req * a.cap;
@@ -857,9 +926,28 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 1, 4>, stream_smem<32, 1>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<64, 2, 3>, stream_smem<64, 3>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 4>, stream_smem<32, 4>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_seed<256, 4, kModeShardEmit>, stream_smem<32, 4>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 2, 3, kModeStats>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 2, 3, kModeShardEmit>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 2>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
+}
+
+// Codebook shard phases (V_local = a.Vl columns, <= 8192 per rank in this build).
+cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s) {
+  const int total = a.batch * rows;
+  const int sms = g_num_sms > 0 ? g_num_sms : 148;
+  k_stream<32, 1, 2, 3, kModeStats><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s) {
+  const int total = a.batch * rows;
+  const int sms = g_num_sms > 0 ? g_num_sms : 148;
+  k_seed<256, 4, kModeShardEmit><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+  k_stream<32, 1, 2, 3, kModeShardEmit><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 4);
+  return cudaGetLastError();
 }
 
 // Usable when a row and its mask can be bulk-copied: V % 128 == 0 (16-byte mask rows), V <= 16384.

@@ -380,3 +380,74 @@ def test_c4_full_size_sampled(xgr):
     assert np.all(out["n_live"] == 512)
     cnt = bs.counters()
     assert cnt["overflow"] == 0, cnt
+
+
+# ---- codebook shard, emulated on one GPU ---------------------------------------------
+class ShardEmulator:
+    """G ranks' contexts on one device; the two all-gathers are plain concatenations (the same
+    rank-major layout an NCCL all-gather produces)."""
+
+    def __init__(self, xgr, vocab, nd, bw, batch, G, items, flags=0):
+        self.G, self.vocab = G, vocab
+        self.ranks = [xgr.BeamSearch(vocab, nd, bw, batch, flags=flags, nranks=G, rank=r) for r in range(G)]
+        for bs in self.ranks:
+            bs.mask_build(items)
+        self.bw = bw
+
+    def step(self, logits_full):
+        vl = self.vocab // self.G
+        sl = [logits_full[:, :, r * vl:(r + 1) * vl] for r in range(self.G)]
+        stats = [bs.shard_stats(x) for bs, x in zip(self.ranks, sl)]
+        gstats = torch.stack([s.clone() for s in stats]).contiguous()
+        outs = [bs.shard_select(gstats) for bs in self.ranks]
+        grecs = torch.stack([r.clone() for r, _ in outs]).contiguous()
+        gn = torch.stack([n.clone() for _, n in outs]).contiguous()
+        for bs in self.ranks:
+            bs.shard_merge(grecs, gn)
+        for bs in self.ranks:
+            bs.batch = logits_full.shape[0]
+        torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("vocab,G,n,bw,batch", [(1024, 4, 200000, 64, 3), (1024, 8, 50000, 32, 2),
+                                                 (16384, 2, 20_000_000, 128, 2), (4096, 2, 30000, 16, 3)])
+def test_codebook_shard_emulated_parity(xgr, vocab, G, n, bw, batch):
+    nd = 3
+    if vocab == 16384:
+        items = make_items(n, vocab, nd, 424242)
+    else:
+        rng = np.random.default_rng(vocab + G)
+        items = rng.integers(0, vocab, size=(n, nd)).astype(np.int32)
+    voc = O.Vocabulary(items, vocab, nd)
+    em = ShardEmulator(xgr, vocab, nd, bw, batch, G, items)
+    hist_p, hist_t = [], []
+    sc = nl = None
+    for t in range(nd):
+        x = torch.from_numpy(make_logits((batch, 1 if t == 0 else bw, vocab), 300 + t, 2.0)).cuda()
+        if t == 0:
+            states = [O.BeamState.root() for _ in range(batch)]
+        else:
+            states = [O.state_from_history([h[r] for h in hist_p], [h[r] for h in hist_t], sc[r], nl[r])
+                      for r in range(batch)]
+        em.step(x)
+        views = [bs.view() for bs in em.ranks]
+        par = views[0]["parent"].cpu().numpy().copy()
+        tok = views[0]["token"].cpu().numpy().copy()
+        sc = views[0]["score"].cpu().numpy().copy()
+        nl = views[0]["n_live"].cpu().numpy().copy()
+        for v in views[1:]:   # every rank commits the identical state
+            assert np.array_equal(v["parent"].cpu().numpy(), par)
+            assert np.array_equal(v["score"].cpu().numpy(), sc)
+        for r in range(batch):
+            compare_step(voc, states[r], x[r].cpu().numpy(), bw, par[r], tok[r], sc[r], nl[r],
+                         where=f"shard G={G} req {r} step {t + 1}")
+        hist_p.append(par)
+        hist_t.append(tok)
+    outs = [bs.finalize(on_device=False) for bs in em.ranks]
+    for o in outs[1:]:
+        for k in o:
+            assert np.array_equal(o[k], outs[0][k])
+    for r in range(batch):
+        for j in range(int(outs[0]["n_live"][r])):
+            tup = tuple(int(a) for a in outs[0]["tokens"][r, j])
+            assert voc.item_rank(tup) == int(outs[0]["item_rank"][r, j])

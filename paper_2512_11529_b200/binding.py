@@ -379,9 +379,10 @@ class ShardedBeamSearch:
     def _dist_all_gather(self, t):
         import torch
         import torch.distributed as dist
-        out = torch.empty((self.bs.nranks, *t.shape), dtype=t.dtype, device=t.device)
-        dist.all_gather_into_tensor(out, t.contiguous(), group=self.group)
-        return out
+        t = t.contiguous()
+        out = torch.empty((self.bs.nranks * t.shape[0], *t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t, group=self.group)   # concatenated along dim 0
+        return out.view(self.bs.nranks, *t.shape)
 
     def step(self, logits_local, stream=None):
         stats = self.bs.shard_stats(logits_local, stream)

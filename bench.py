@@ -179,7 +179,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     t0 = time.perf_counter()
     items = make_items(cfg["n_items"], V, ND, cfg["trie_key"])
     gen_s = time.perf_counter() - t0
-    bs = xgr.BeamSearch(V, ND, BW, B, device=local_rank, flags=xgr.XGR_CFG_TIMING)
+    bs = xgr.BeamSearch(V, ND, BW, B, device=local_rank, flags=xgr.XGR_CFG_TIMING,
+                        theta_rows=int(os.environ.get("XGR_THETA_ROWS", "0")))
     t0 = time.perf_counter()
     bs.mask_build(items)
     torch.cuda.synchronize()
@@ -258,7 +259,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if rank == 0 and not args.profile:
         # ---- accounting + counters on an identical, untimed pass (separate ctx) ----
-        acc = xgr.BeamSearch(V, ND, BW, B, device=local_rank, flags=xgr.XGR_CFG_COUNTERS)
+        acc = xgr.BeamSearch(V, ND, BW, B, device=local_rank, flags=xgr.XGR_CFG_COUNTERS,
+                             theta_rows=int(os.environ.get("XGR_THETA_ROWS", "0")))
         acc.mask_build(items)
         acc.counters()
         algb = None

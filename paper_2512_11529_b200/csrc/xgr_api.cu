@@ -42,6 +42,7 @@ struct xgr_ctx {
   int32_t** d_phist = nullptr;     // device array of nd pointers
   int32_t** d_thist = nullptr;
   uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
+  uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
   uint64_t* surv = nullptr;        // [maxB][cap]
   float* lse = nullptr;            // [maxB][BW]
   uint32_t* flags = nullptr;       // [maxB]
@@ -104,6 +105,7 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->d_phist);
   cudaFree(c->d_thist);
   cudaFree(c->scratch);
+  cudaFree(c->seed_hist);
   cudaFree(c->surv);
   cudaFree(c->lse);
   cudaFree(c->flags);
@@ -184,6 +186,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->d_phist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->d_thist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->scratch, 3 * (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
+  if (e == cudaSuccess) e = cudaMemset(x->seed_hist, 0, (size_t)x->maxB * kSeedBins * 4);
   if (e == cudaSuccess) e = al((void**)&x->surv, (size_t)x->maxB * x->cap * 8);
   if (e == cudaSuccess) e = al((void**)&x->lse, nb * 4);
   if (e == cudaSuccess) e = al((void**)&x->flags, (size_t)x->maxB * 4);
@@ -294,6 +298,7 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const float* logits, in
   a.theta = ctx->scratch;
   a.surv_count = ctx->scratch + ctx->maxB;
   a.ovf = ctx->scratch + 2 * ctx->maxB;
+  a.seed_hist = ctx->seed_hist;
   a.surv = ctx->surv;
   a.lse = ctx->lse;
   a.flags = ctx->flags;

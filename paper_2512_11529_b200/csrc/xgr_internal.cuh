@@ -13,6 +13,7 @@ namespace xgr {
 constexpr int kMaxND = 8;
 constexpr int kMaxBW = 1024;
 constexpr int kSparseCap = 16384;   // max candidates per request the sparse-step kernel holds
+constexpr int kSeedBins = 2048;     // histogram seed: bins of 1/128 over S_0 - c in [0, 16)
 
 // ---- trie, one entry per level d = 0..nd (level d = nodes for prefixes of length d) ----------
 struct LevelDev {
@@ -75,6 +76,7 @@ struct StepArgs {
   uint32_t* theta;      // orderable(theta), 0 = no bound (-inf)
   uint32_t* surv_count;
   uint32_t* ovf;        // this step's overflow marker
+  uint32_t* seed_hist;  // [batch][kSeedBins] histogram of S_0 - c over the seed rows (zero between steps)
   uint64_t* surv;       // [batch][cap] survivor keys
   float* lse;           // [batch][BW] per-row lse (NaN: row not read)
   uint32_t* flags;      // sticky per-request status bits

@@ -462,6 +462,173 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 }
 
 // ------------------------------------------------------------------------------------------
+// Histogram seed (default): theta from the union of rows 0..R0-1 without holding them in one CTA.
+// Every candidate of a request is <= S_0 (slot scores are sorted and logp <= 0), so the distances
+// d = S_0 - c share one grid across rows: k_seed_hist (one CTA per seed row) adds its row's
+// candidates to a per-request histogram of d (bins of 1/128) -- only those >= a row-local bound
+// that keeps at least BW of the row's candidates --, and k_seed_theta takes the first bin where the
+// count reaches BW: theta = S_0 - (bin + 1) / 128 - margin has >= BW candidates above it, so it is
+// <= the request's BW-th best score. The seed rows are then streamed like any other row.
+// ------------------------------------------------------------------------------------------
+template <int T, int VPT>
+__global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
+  constexpr int NW = T / 32;
+  __shared__ float2 part[NW];
+  __shared__ float s_tau[NW];
+  __shared__ uint32_t s_hist[kSeedBins];
+  const int req = blockIdx.x, r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (r >= nlive_of(a, req)) return;
+  float S;
+  uint32_t node;
+  row_state(a, req, r, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  const int slot = L.dense_slot ? L.dense_slot[node] : -1;
+  if (slot < 0) return;   // sparse seed rows contribute nothing (no bound from them)
+  const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
+  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
+  const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W + (a.col0 >> 5);
+  const int Vl = a.Vl;
+  float x[4 * VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int q = i * T + tid;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t nb = 0;
+    if (4 * q < Vl) {
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(row + 4 * q));
+      nb = (__ldg(bm + (q >> 3)) >> (4 * (q & 7))) & 0xFu;
+    }
+    x[4 * i] = (nb & 1u) ? v.x : -INFINITY;
+    x[4 * i + 1] = (nb & 2u) ? v.y : -INFINITY;
+    x[4 * i + 2] = (nb & 4u) ? v.z : -INFINITY;
+    x[4 * i + 3] = (nb & 8u) ? v.w : -INFINITY;
+  }
+  float lse;
+  if (a.gstats) {   // codebook shard: the global lse from all ranks' stats
+    bool fin;
+    lse = shard_lse(a, req, r, fin);
+    if (!fin) return;
+  } else {
+    float tmax = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 4 * VPT; ++e) tmax = fmaxf(tmax, x[e]);
+    const float mw = wmax(tmax);
+    const float mws = mw == -INFINITY ? 0.f : mw;
+    float z = 0.f;
+#pragma unroll
+    for (int e = 0; e < 4 * VPT; ++e) z += ex2f(__fmul_rn(__fsub_rn(x[e], mws), kLog2eS));
+    const float zw = wsum(z);
+    if (lane == 0) part[warp] = make_float2(mw, zw);
+    __syncthreads();
+    float M = part[0].x;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) M = fmaxf(M, part[w].x);
+    float Z = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) Z += part[w].y * ex2f(__fmul_rn(__fsub_rn(part[w].x, M), kLog2eS));
+    if (!((Z > 0.5f) && (Z <= 3.0e38f))) return;   // k_stream flags non-finite rows
+    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+  }
+  float cmax = -INFINITY;
+#pragma unroll
+  for (int e = 0; e < 4 * VPT; ++e) {
+    x[e] = cand_score(S, x[e], lse);
+    cmax = fmaxf(cmax, x[e]);
+  }
+  // row-local bound keeping >= BW candidates: the m-th largest thread max of each warp
+  // (m = ceil(BW / warps)), minimised over warps
+  const int m = (a.BW + NW - 1) / NW;
+  float tau = -INFINITY;
+  if (m <= 32) {
+    float v = cmax;
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        const float o = __shfl_xor_sync(0xffffffffu, v, stride);
+        const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
+        v = keep_max ? fmaxf(v, o) : fminf(v, o);
+      }
+    }
+    const float wm = __shfl_sync(0xffffffffu, v, m - 1);
+    if (lane == 0) s_tau[warp] = wm;
+    __syncthreads();
+    tau = s_tau[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) tau = fminf(tau, s_tau[w]);
+  }
+  // shared-memory histogram first, then one global add per non-empty bin
+  for (int i = tid; i < kSeedBins; i += T) s_hist[i] = 0u;
+  __syncthreads();
+  if (cmax >= tau && cmax > -INFINITY) {
+#pragma unroll
+    for (int e = 0; e < 4 * VPT; ++e) {
+      if (x[e] >= tau && x[e] > -INFINITY) {
+        const float dd = __fmul_rn(__fsub_rn(S0, x[e]), 128.0f);
+        if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(&s_hist[(int)dd], 1u);
+      }
+    }
+  }
+  __syncthreads();
+  uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+  for (int i = tid; i < kSeedBins; i += T) {
+    const uint32_t v = s_hist[i];
+    if (v) atomicAdd(h + i, v);
+  }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepArgs a) {
+  constexpr int PER = kSeedBins / T;
+  __shared__ uint32_t s_w[T / 32];
+  __shared__ int s_bin;
+  const int req = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+  uint32_t c[PER], loc = 0;
+#pragma unroll
+  for (int j = 0; j < PER; ++j) {
+    c[j] = h[tid * PER + j];
+    loc += c[j];
+  }
+#pragma unroll
+  for (int j = 0; j < PER; ++j) h[tid * PER + j] = 0u;   // ready for the next dense step
+  uint32_t incl = loc;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_w[tid >> 5] = incl;
+  if (tid == 0) s_bin = -1;
+  __syncthreads();
+  uint32_t off = 0;
+  for (int w = 0; w < (tid >> 5); ++w) off += s_w[w];
+  incl += off;
+  uint32_t acc = incl - loc;
+  const uint32_t need = (uint32_t)(a.no_prune ? 0x7FFFFFFF : a.BW);
+  if (acc < need && incl >= need) {
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      if (acc < need && acc + c[j] >= need) s_bin = tid * PER + j;
+      acc += c[j];
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint32_t th = 0u;
+    if (s_bin >= 0) {
+      const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
+      const float t = S0 - (float)(s_bin + 1) * (1.0f / 128.0f) - 1e-5f * fmaxf(1.0f, fabsf(S0));
+      th = f2o(t);
+    }
+    a.theta[req] = th;
+    a.surv_count[req] = 0u;
+    a.ovf[req] = 0u;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
 // k_stream: G consumer groups of 256 threads (thread t of a group owns EPT consecutive tokens,
 // EPT/32 mask words) process different rows concurrently; one producer warp feeds them.
 // ------------------------------------------------------------------------------------------
@@ -908,6 +1075,7 @@ static size_t stream_smem() {
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
+static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>
 static cudaError_t opt_in(K k, size_t smem) {
@@ -931,6 +1099,7 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeShardEmit>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 2>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
+  if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
@@ -961,9 +1130,20 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
   if (a.trie.V <= 8192) {
-    const int seeded = g_seed_rows == 2 ? 2 : 4;
-    if (seeded == 2) k_seed<256, 2><<<a.batch, 512, stream_smem<32, 2>(), s>>>(a);
-    else k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+    int seeded = g_seed_rows == 2 ? 2 : 4;
+    if (g_seed_mode == 1) {   // histogram seed over rows 0..R0-1; every row is then streamed
+      const int r0 = std::min(a.theta_rows, rows);
+      if (r0 > 0) {
+        k_seed_hist<256, 8><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+        ++*launches;
+      }
+      k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+      seeded = 0;
+    } else if (seeded == 2) {
+      k_seed<256, 2><<<a.batch, 512, stream_smem<32, 2>(), s>>>(a);
+    } else {
+      k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+    }
     if (ev0) cudaEventRecord(ev0, s);
     switch (g_stream_variant) {
       case 1:   // one CTA per SM: one producer feeding three consumer groups from a 6-stage ring

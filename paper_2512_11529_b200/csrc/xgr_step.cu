@@ -346,6 +346,81 @@ __device__ void block_select_topk(const uint64_t* keys, int n, int k, uint64_t* 
   sort_desc_to<T>(sel, k, out);
 }
 
+// Bitonic sort (descending) of n <= T * EPT distinct nonzero keys; the first k_out go to out.
+// Thread t holds elements EPT*t .. EPT*t + EPT - 1 in registers: strides < EPT are exchanged in
+// registers, strides < 32 * EPT by warp shuffles, larger ones through xbuf (T * EPT keys; may be
+// src itself) with one barrier on each side -- 10 barrier pairs for 2048 keys.
+template <int T, int EPT>
+__device__ void block_sort_desc(const uint64_t* src, int n, uint64_t* xbuf, uint64_t* out, int k_out) {
+  constexpr int N = T * EPT;
+  const int tid = threadIdx.x;
+  uint64_t v[EPT];
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int i = EPT * tid + j;
+    v[j] = i < n ? src[i] : 0ull;   // padding 0 sorts last
+  }
+  __syncthreads();
+#pragma unroll
+  for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride < EPT) {
+#pragma unroll
+        for (int s2 = 1; s2 < EPT; s2 <<= 1) {   // compile-time register indices only
+#pragma unroll
+          for (int j = 0; j < EPT; ++j) {
+            if (s2 == stride && (j & s2) == 0) {
+              const int jj = j | s2;
+              const bool desc = ((EPT * tid + j) & size) == 0;
+              const uint64_t hi = v[j] > v[jj] ? v[j] : v[jj];
+              const uint64_t lo = v[j] > v[jj] ? v[jj] : v[j];
+              v[j] = desc ? hi : lo;
+              v[jj] = desc ? lo : hi;
+            }
+          }
+        }
+      } else if (stride < 32 * EPT) {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const int i = EPT * tid + j;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[j], stride / EPT);
+          const bool keep_max = ((i & stride) == 0) == ((i & size) == 0);
+          v[j] = keep_max ? (o > v[j] ? o : v[j]) : (o < v[j] ? o : v[j]);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) xbuf[EPT * tid + j] = v[j];
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const int i = EPT * tid + j;
+          const uint64_t o = xbuf[i ^ stride];
+          const bool keep_max = ((i & stride) == 0) == ((i & size) == 0);
+          v[j] = keep_max ? (o > v[j] ? o : v[j]) : (o < v[j] ? o : v[j]);
+        }
+        __syncthreads();
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < EPT; ++j) {
+    const int i = EPT * tid + j;
+    if (i < k_out) out[i] = v[j];
+  }
+  __syncthreads();
+}
+
+// Top-k of n <= T keys by a full block sort (cand: >= T keys of exchange space; may be keys).
+// One key per thread only: the unrolled network for 2-4 keys per thread was measured slower.
+template <int T>
+__device__ bool block_sort_topk(const uint64_t* keys, int n, int k, uint64_t* cand, int cand_cap,
+                                uint64_t* out) {
+  if (n > T || cand_cap < T) return false;
+  block_sort_desc<T, 1>(keys, n, cand, out, k);
+  return true;
+}
+
 // Fast top-k of distinct keys in shared memory (used by the per-request select kernels).
 // Threshold without atomics or passes: every thread takes the max of its keys; each warp sorts
 // its 32 maxima (shuffle bitonic) and takes the m-th largest, m = ceil(k / warps); the minimum of
@@ -362,11 +437,12 @@ struct TopkScratch {
 
 template <int T>
 __device__ int block_topk_fast(uint64_t* keys, int n, int k, uint64_t* cand, int cand_cap,
-                               uint64_t* sel, uint64_t* out, TopkScratch& sc) {
+                               uint64_t* sel, uint64_t* out, TopkScratch& sc, int a_dbg_sort = 0) {
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   constexpr int NW = T / 32;
   if (k <= 0) return 0;
   const int m = (k + NW - 1) / NW;
+  if (!(a_dbg_sort & 1) && block_sort_topk<T>(keys, n, k, cand, cand_cap, out)) return k;
   if (n <= 2 * k || m > 32) {
     block_select_topk<T>(keys, n, k, sel, out, sc.hist, sc.m64, sc.m32);
     return k;
@@ -409,6 +485,7 @@ __device__ int block_topk_fast(uint64_t* keys, int n, int k, uint64_t* cand, int
   }
   __syncthreads();
   const int nc = (int)sc.n_c;
+  if (nc <= cand_cap && !(a_dbg_sort & 1) && block_sort_topk<T>(cand, nc, k, cand, cand_cap, out)) return k;
   if (nc > cand_cap) block_select_topk<T>(keys, n, k, sel, out, sc.hist, sc.m64, sc.m32);
   else block_select_topk<T>(cand, nc, k, sel, out, sc.hist, sc.m64, sc.m32);
   return k;
@@ -839,7 +916,15 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   __shared__ TopkScratch s_sc;
   __shared__ ParentInfo s_pi;
   const int req = blockIdx.x, tid = threadIdx.x;
+  const uint64_t* src = a.surv + (size_t)req * a.cap;
+  const uint64_t p0 = tid < a.cap ? src[tid] : 0ull;
+  const uint64_t p1 = tid + T < a.cap ? src[tid + T] : 0ull;
+  const size_t pb = (size_t)req * a.BW;
+  const uint32_t nd0 = (a.node_in && tid < a.BW) ? a.node_in[pb + tid] : 0u;
+  const uint32_t nd1 = (a.node_in && tid + T < a.BW) ? a.node_in[pb + tid + T] : 0u;
+  const int nl = nlive_of(a, req);
   const uint32_t n = a.surv_count[req];
+  static_assert(2 * T >= kMaxBW, "k_select: parents prefetched two per thread");
   if (n > (uint32_t)a.cap) {
     // the survivor buffer overflowed (weak theta, massive ties): exact multi-pass fallback
     if (tid == 0) {
@@ -853,12 +938,27 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
     return;
   }
   const int k = min((int)n, a.BW);
-  const uint64_t* src = a.surv + (size_t)req * a.cap;
-  for (uint32_t i = tid; i < n; i += T) s_keys[i] = src[i];
-  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
+  // survivors 0..2T-1 and the parents' beam state were loaded speculatively above, alongside
+  // the count and nlive, so each chain is one load shorter
+  if ((uint32_t)tid < n) s_keys[tid] = p0;
+  if ((uint32_t)(tid + T) < n) s_keys[tid + T] = p1;
+  for (uint32_t i = tid + 2 * T; i < n; i += T) s_keys[i] = src[i];
+  {
+    const LevelDev& L = a.trie.lv[a.level];
+    if (tid < nl) {
+      s_pi.fc[tid] = L.first_child[nd0];
+      s_pi.fcn[tid] = L.first_child[nd0 + 1];
+      s_pi.slot[tid] = L.dense_slot ? L.dense_slot[nd0] : -1;
+    }
+    if (tid + T < nl) {
+      s_pi.fc[tid + T] = L.first_child[nd1];
+      s_pi.fcn[tid + T] = L.first_child[nd1 + 1];
+      s_pi.slot[tid + T] = L.dense_slot ? L.dense_slot[nd1] : -1;
+    }
+  }
   __syncthreads();
   if (a.dbg & 128) return;
-  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
   if (a.dbg & 256) return;
   commit<T>(a, req, s_out, k, s_pi);
 }
@@ -897,7 +997,7 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
   }
   __syncthreads();
   const int k = min(n, a.BW);
-  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
   commit<T>(a, req, s_out, k, s_pi);
 }
 
@@ -919,6 +1019,16 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   __shared__ uint32_t s_count, s_nbig;
   __shared__ int32_t s_big[kMaxBW];
   const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
+  // beam state of rows tid and tid + T loaded speculatively, alongside nlive
+  static_assert(2 * T >= kMaxBW, "k_sparse: two rows per thread");
+  float S_pre[2];
+  uint32_t node_pre[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    S_pre[u] = 0.f;
+    node_pre[u] = 0u;
+    if (!ROOT && tid + u * T < a.BW) row_state(a, req, tid + u * T, S_pre[u], node_pre[u]);
+  }
   const int nl = nlive_of(a, req);
   const LevelDev& L = a.trie.lv[a.level];
   const uint16_t* lab = a.trie.lv[a.level + 1].label;
@@ -927,7 +1037,9 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
     s_count = 0;
     s_nbig = 0;
   }
-  prefetch_parents<T>(a, req, nl, s_pi);
+  // the commit's parent info (first child, end, dense slot) is written by the gather below,
+  // which loads the same node data; the barriers before the commit order it
+  if (ROOT) prefetch_parents<T>(a, req, nl, s_pi);
   __syncthreads();
   if (ROOT) {
     constexpr int RPT = 16;   // root children held in registers per thread (<= 8192 children)
@@ -995,11 +1107,16 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
     }
   } else {
     constexpr int kSmall = 16;
-    for (int b = tid; b < nl; b += T) {
-      float S;
-      uint32_t node;
-      row_state(a, req, b, S, node);
+#pragma unroll 1
+    for (int u = 0; u < 2; ++u) {
+      const int b = tid + u * T;
+      if (b >= nl) break;
+      const float S = u ? S_pre[1] : S_pre[0];
+      const uint32_t node = u ? node_pre[1] : node_pre[0];
       const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      s_pi.fc[b] = fc;
+      s_pi.fcn[b] = fe;
+      s_pi.slot[b] = L.dense_slot ? L.dense_slot[node] : -1;
       const int cnt = (int)(fe - fc);
       if (cnt > kSmall) {
         s_big[atomicAdd(&s_nbig, 1u)] = b;
@@ -1060,7 +1177,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   const int n = (int)s_count;
   if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
   const int k = min(n, a.BW);
-  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc);
+  block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
   commit<T>(a, req, s_out, k, s_pi);
 }
 

@@ -477,32 +477,38 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   __shared__ float s_tau[NW];
   __shared__ uint32_t s_hist[kSeedBins];
   const int req = blockIdx.x, r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (r >= nlive_of(a, req)) return;
+  // The row (always in bounds: r < rows) and the beam state are loaded up front and together;
+  // only the dense slot and then its bitmap depend on earlier loads.
+  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
+  const int Vl = a.Vl;
+  float4 v[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int q = i * T + tid;
+    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (4 * q < Vl)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                   : "=f"(v[i].x), "=f"(v[i].y), "=f"(v[i].z), "=f"(v[i].w) : "l"(row + 4 * q));
+  }
+  const int nl = nlive_of(a, req);
   float S;
   uint32_t node;
   row_state(a, req, r, S, node);
+  const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
+  if (r >= nl) return;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   if (slot < 0) return;   // sparse seed rows contribute nothing (no bound from them)
-  const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
-  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
   const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W + (a.col0 >> 5);
-  const int Vl = a.Vl;
   float x[4 * VPT];
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
     const int q = i * T + tid;
-    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-    uint32_t nb = 0;
-    if (4 * q < Vl) {
-      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                   : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(row + 4 * q));
-      nb = (__ldg(bm + (q >> 3)) >> (4 * (q & 7))) & 0xFu;
-    }
-    x[4 * i] = (nb & 1u) ? v.x : -INFINITY;
-    x[4 * i + 1] = (nb & 2u) ? v.y : -INFINITY;
-    x[4 * i + 2] = (nb & 4u) ? v.z : -INFINITY;
-    x[4 * i + 3] = (nb & 8u) ? v.w : -INFINITY;
+    const uint32_t nb = (4 * q < Vl) ? (__ldg(bm + (q >> 3)) >> (4 * (q & 7))) & 0xFu : 0u;
+    x[4 * i] = (nb & 1u) ? v[i].x : -INFINITY;
+    x[4 * i + 1] = (nb & 2u) ? v[i].y : -INFINITY;
+    x[4 * i + 2] = (nb & 4u) ? v[i].z : -INFINITY;
+    x[4 * i + 3] = (nb & 8u) ? v[i].w : -INFINITY;
   }
   float lse;
   if (a.gstats) {   // codebook shard: the global lse from all ranks' stats

@@ -62,6 +62,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -75,10 +80,11 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Warp max in one instruction (sm_100a redux.sync .f32; NaN inputs are ignored, as by fmaxf).
 __device__ __forceinline__ float wmax(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
 }
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
@@ -690,6 +696,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     // batch n+1, and the copies of batch n, so no round trip is exposed between batches.
     const int lane = tid & 31;
     const uint64_t pol = policy_evict_first();
+    const uint64_t pol_keep = policy_evict_last();
     struct Meta {
       int b, req, live;
       float S, th;
@@ -777,7 +784,9 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
             const uint32_t rb = (uint32_t)a.Vl * 4u, mb = (uint32_t)(a.Vl >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
             bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
-            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (a.col0 >> 5), mb, &full[st], pol);
+            // a dense node's bitmap is shared by every row whose beam sits on it: keep it in L2
+            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (a.col0 >> 5), mb, &full[st],
+                     pol_keep);
           } else {
             mbar_arrive(&full[st]);
           }
@@ -957,14 +966,11 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     named_sync(bar_id, GT);
     ++it;
     float2 pr = lane < GT / 32 ? pp[lane] : make_float2(-INFINITY, 0.f);
-    float M = pr.x;
-#pragma unroll
-    for (int o = GT / 64; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    const float M = wmax(pr.x);   // warp-uniform
     float zi = pr.y * ex2f(__fmul_rn(__fsub_rn(pr.x, M), kLog2eS));
     if (lane >= GT / 32) zi = 0.f;
 #pragma unroll
     for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
-    M = __shfl_sync(0xffffffffu, M, 0);
     const float Z = __shfl_sync(0xffffffffu, zi, 0);
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
       if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);

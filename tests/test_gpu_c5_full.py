@@ -1,0 +1,80 @@
+"""C5 at full size: 1B-item trie, V = 65536, BW = 512, batch 128, ND = 3, codebook-sharded over
+G = 8 rank contexts (8192 columns each) emulated on one GPU (tests/shard_emu.py), sampled requests
+checked against the teacher-forced oracle at every step, every rank's state bitwise identical.
+
+Heavy-ish: 1B items (~50 GB host RAM peak for the generator and the oracle's sorted key list),
+8 tries plus 17 GB of logits per step in HBM; ~2.5 min on a B200 box (log in
+profiles/r01_c5_full_parity.log). XGR_SKIP_C5=1 skips it.
+"""
+import os
+import time
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("XGR_SKIP_C5") == "1", reason="XGR_SKIP_C5=1")]
+
+from oracle import xbeam_oracle as O  # noqa: E402
+from synth import config, make_items, make_logits_torch  # noqa: E402
+from tests.parity import compare_step  # noqa: E402
+from tests.shard_emu import ShardEmulator  # noqa: E402
+
+
+def test_c5_full_size_codebook_shard():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2512_11529_b200 as xgr
+    c = config("C5")
+    V, nd, bw, B, G = c["vocab"], c["nd"], c["beam_width"], c["batch"], 8
+    check = [0, 64, 127]
+    t0 = time.time()
+    items = make_items(c["n_items"], V, nd, c["trie_key"])
+    t_gen = time.time() - t0
+    voc = O.Vocabulary(items, V, nd)
+    assert voc.n_items == c["n_items"]
+    t_voc = time.time() - t0 - t_gen
+    em = ShardEmulator(xgr, V, nd, bw, B, G, items)
+    del items
+    t_build = time.time() - t0 - t_gen - t_voc
+    hist_p, hist_t = [], []
+    sc = nl = None
+    res = {"strict": 0, "adjudicated": 0}
+    t_steps = []
+    for t in range(nd):
+        x = make_logits_torch((B, 1 if t == 0 else bw, V), 11 * t + 5, 2.0)
+        if t == 0:
+            states = {r: O.BeamState.root() for r in check}
+        else:
+            states = {r: O.state_from_history([h[r] for h in hist_p], [h[r] for h in hist_t], sc[r], nl[r])
+                      for r in check}
+        ts = time.time()
+        em.step(x)
+        t_steps.append(time.time() - ts)
+        views = [bs.view() for bs in em.ranks]
+        par = views[0]["parent"].cpu().numpy().copy()
+        tok = views[0]["token"].cpu().numpy().copy()
+        sc = views[0]["score"].cpu().numpy().copy()
+        nl = views[0]["n_live"].cpu().numpy().copy()
+        for v in views[1:]:   # every rank commits the identical state
+            assert np.array_equal(v["parent"].cpu().numpy(), par)
+            assert np.array_equal(v["token"].cpu().numpy(), tok)
+            assert np.array_equal(v["score"].cpu().numpy(), sc)
+        for r in check:
+            res[compare_step(voc, states[r], x[r].cpu().numpy(), bw, par[r], tok[r], sc[r], nl[r],
+                             where=f"C5 req {r} step {t + 1}")] += 1
+        hist_p.append(par)
+        hist_t.append(tok)
+        del x
+    outs = [bs.finalize(on_device=False) for bs in em.ranks]
+    for o in outs[1:]:
+        for k in o:
+            assert np.array_equal(o[k], outs[0][k])
+    assert np.all(outs[0]["n_live"] == bw)
+    for r in check:
+        for j in range(bw):
+            tup = tuple(int(a) for a in outs[0]["tokens"][r, j])
+            assert voc.item_rank(tup) == int(outs[0]["item_rank"][r, j])
+    print(f"\nC5 full: items {t_gen:.1f} s, oracle vocabulary {t_voc:.1f} s, 8 tries {t_build:.1f} s, "
+          f"steps {['%.2f s' % s for s in t_steps]} (untimed emulation), checks {res}")

@@ -13,6 +13,7 @@ pytestmark = pytest.mark.gpu
 from oracle import xbeam_oracle as O  # noqa: E402
 from synth import config, make_items, make_logits, make_logits_torch, prefix_keyed_row  # noqa: E402
 from tests.parity import compare_step  # noqa: E402
+from tests.shard_emu import ShardEmulator  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -383,32 +384,6 @@ def test_c4_full_size_sampled(xgr):
 
 
 # ---- codebook shard, emulated on one GPU ---------------------------------------------
-class ShardEmulator:
-    """G ranks' contexts on one device; the two all-gathers are plain concatenations (the same
-    rank-major layout an NCCL all-gather produces)."""
-
-    def __init__(self, xgr, vocab, nd, bw, batch, G, items, flags=0):
-        self.G, self.vocab = G, vocab
-        self.ranks = [xgr.BeamSearch(vocab, nd, bw, batch, flags=flags, nranks=G, rank=r) for r in range(G)]
-        for bs in self.ranks:
-            bs.mask_build(items)
-        self.bw = bw
-
-    def step(self, logits_full):
-        vl = self.vocab // self.G
-        sl = [logits_full[:, :, r * vl:(r + 1) * vl] for r in range(self.G)]
-        stats = [bs.shard_stats(x) for bs, x in zip(self.ranks, sl)]
-        gstats = torch.stack([s.clone() for s in stats]).contiguous()
-        outs = [bs.shard_select(gstats) for bs in self.ranks]
-        grecs = torch.stack([r.clone() for r, _ in outs]).contiguous()
-        gn = torch.stack([n.clone() for _, n in outs]).contiguous()
-        for bs in self.ranks:
-            bs.shard_merge(grecs, gn)
-        for bs in self.ranks:
-            bs.batch = logits_full.shape[0]
-        torch.cuda.synchronize()
-
-
 @pytest.mark.parametrize("vocab,G,n,bw,batch", [(1024, 4, 200000, 64, 3), (1024, 8, 50000, 32, 2),
                                                  (16384, 2, 20_000_000, 128, 2), (4096, 2, 30000, 16, 3)])
 def test_codebook_shard_emulated_parity(xgr, vocab, G, n, bw, batch):

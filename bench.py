@@ -132,9 +132,10 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def committed_traffic():
+def committed_traffic(dtype="f32"):
     """dram bytes per launch of k_stream from the committed ncu --set full summary, if any."""
-    p = os.path.join(ROOT, "profiles", "ncu_k_stream_traffic.json")
+    p = os.path.join(ROOT, "profiles", "ncu_k_stream_traffic.json" if dtype == "f32"
+                     else f"ncu_k_stream_{dtype}_traffic.json")
     try:
         with open(p) as f:
             return json.load(f)
@@ -189,7 +190,9 @@ def run_ours(args, cfg, rank, world, local_rank):
     seeds = step_seeds(plan, ND)
     logits = [make_logits_torch((B, 1 if t == 0 else BW, V), seeds[t], args.sigma, device=dev)
               for t in range(ND)]
-    in_bytes = sum(x.numel() * 4 for x in logits)
+    if args.logits == "bf16":   # NEXT f1: the same N(0, sigma^2) draws rounded to bf16
+        logits = [x.to(torch.bfloat16) for x in logits]
+    in_bytes = sum(x.numel() * x.element_size() for x in logits)
     stream = torch.cuda.current_stream()
     out = {"tokens": torch.empty((B, BW, ND), dtype=torch.int32, device=dev),
            "item_rank": torch.empty((B, BW), dtype=torch.int64, device=dev),
@@ -245,8 +248,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "warmup": args.warmup, "ms_per_step": total_ms_max / args.steps,
         "p50_ms": statistics.median(per_iter), "p99_ms": sorted(per_iter)[min(len(per_iter) - 1, int(0.99 * len(per_iter)))],
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded: Feistel-permuted uniform item tuples, N(0, sigma^2) fp32 logits)",
+        "data": f"synthetic (seeded: Feistel-permuted uniform item tuples, N(0, sigma^2) {args.logits} logits)",
         "config": {"workload": cfg["name"], "batch_per_gpu": B, "beam_width": BW, "vocab": V, "nd": ND,
+                   "logits": args.logits,
                    "n_items": cfg["n_items"], "n_items_dedup": int(info["n_items"]), "sigma": args.sigma,
                    "parallelism": f"request-split x{world}",
                    "l2": f"inputs larger than L2 ({in_bytes / 2**30:.2f} GiB per pass), no flush"},
@@ -280,7 +284,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             mean_ms = sum(main_ms) / len(main_ms)
             achieved = algb["alg_bytes"] / (mean_ms / 1e3) / 1e9
             step_dense = statistics.median(per_step[dense_steps[0] - 1]) if dense_steps else None
-            tr = committed_traffic()
+            tr = committed_traffic(args.logits)
             res["roofline"] = {
                 "bound": "hbm", "kernel": "k_stream (dense step: TMA row stream, masked log-softmax, score add, pruned emit)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -303,7 +307,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     if not args.no_e2e:
         # ---- end to end through the public API: pinned host logits in, host results out ----
         hl = [x.cpu().pin_memory() for x in logits]
-        h2d = sum(x.numel() * 4 for x in hl)
+        h2d = sum(x.numel() * x.element_size() for x in hl)
         d2h = B * BW * ND * 4 + B * BW * 8 + B * BW * 4 + B * 4
         ke = max(1, min(args.steps, 5))
 
@@ -342,7 +346,7 @@ def cpu_baseline(args, cfg, items, logits):
 
     def lf(r, t):
         if (r, t) not in host:
-            host[(r, t)] = logits[t][r].cpu().numpy()
+            host[(r, t)] = logits[t][r].float().cpu().numpy()   # bf16 widened exactly
         return host[(r, t)]
 
     # estimate with one request, then size the sample to ~args.cpu_budget seconds
@@ -397,6 +401,8 @@ def main(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C3")
     ap.add_argument("--sigma", type=float, default=2.0)
+    ap.add_argument("--logits", choices=["f32", "bf16"], default="f32",
+                    help="logits element type (bf16: SURVEY 8(f) NEXT f1); the path computes in f32")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

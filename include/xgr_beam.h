@@ -110,6 +110,19 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
 xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows,
                          int64_t ld, void* stream);
 
+/* Logit element types for xgr_beam_step_ex. */
+#define XGR_DTYPE_F32 0
+#define XGR_DTYPE_BF16 1
+
+/* xgr_beam_step with the logits' element type given (PAPER.md L361, L376
+ * leave the dtype open). XGR_DTYPE_BF16: DEVICE bf16 [batch][rows][ld], 16-byte aligned rows
+ * (ld % 8 == 0); every value is widened exactly to fp32 and the step computes in fp32 as for
+ * XGR_DTYPE_F32 (the oracle widens the same values). bf16 needs V % 128 == 0 and V <= 16384 for
+ * dense steps (the streaming kernels); otherwise XGR_ERR_UNSUPPORTED, as for any other dtype or
+ * a sharded ctx. XGR_DTYPE_F32 is exactly xgr_beam_step. */
+xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype,
+                            int32_t rows, int64_t ld, void* stream);
+
 /* After exactly nd steps: item tuples of the final beams, in slot order (score descending).
  * The last step's kernels already wrote them into ctx-owned device buffers (fused finalize);
  * this call copies them out (device->device or device->host) and resets the ctx. With

@@ -12,6 +12,8 @@ from .binding import (  # noqa: F401
     XGR_CFG_NO_PRUNE,
     XGR_CFG_NO_SPARSE_KERNEL,
     XGR_CFG_TIMING,
+    XGR_DTYPE_BF16,
+    XGR_DTYPE_F32,
     lib,
     LIB_PATH,
 )

@@ -27,7 +27,7 @@ COUNTER_NAMES = ["rows_read", "rows_skip_pre", "rows_skip_post", "legal", "survi
                  "overflow", "sparse_cands", "dense_steps"]
 
 # every symbol include/xgr_beam.h declares
-EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_finalize",
+EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_step_ex", "xgr_beam_finalize",
            "xgr_beam_destroy", "xgr_last_error", "xgr_abi_version", "xgr_beam_view",
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
@@ -62,6 +62,7 @@ def _load():
         "xgr_beam_init": [P(XgrConfig), P(VP)],
         "xgr_mask_build": [VP, VP, I64, VP],
         "xgr_beam_step": [VP, I32, VP, I32, I64, VP],
+        "xgr_beam_step_ex": [VP, I32, VP, I32, I32, I64, VP],
         "xgr_beam_finalize": [VP, VP, VP, VP, VP, I32, VP],
         "xgr_beam_destroy": [VP],
         "xgr_beam_view": [VP, P(VP), P(VP), P(VP), P(VP), P(VP)],
@@ -117,6 +118,13 @@ def xgr_mask_build(ctx, items: np.ndarray, stream=0):
 
 def xgr_beam_step(ctx, batch, logits_ptr, rows, ld, stream=0):
     _check(lib.xgr_beam_step(ctx, batch, logits_ptr, rows, ld, stream))
+
+
+XGR_DTYPE_F32, XGR_DTYPE_BF16 = 0, 1
+
+
+def xgr_beam_step_ex(ctx, batch, logits_ptr, dtype, rows, ld, stream=0):
+    _check(lib.xgr_beam_step_ex(ctx, batch, logits_ptr, dtype, rows, ld, stream))
 
 
 def xgr_beam_finalize(ctx, tokens, item_rank, score, n_live, outputs_on_device, stream=0):
@@ -211,25 +219,26 @@ class BeamSearch:
         return xgr_mask_children(self.ctx, np.asarray(prefixes), depth, cap, self._stream())
 
     def step(self, logits, stream=None):
-        """logits: fp32 [batch][rows][ld] (or [batch][rows][V]); CUDA tensor, or a pinned CPU
-        tensor, which is copied into a device staging buffer on the same stream first."""
+        """logits: fp32 or bf16 [batch][rows][ld] (or [batch][rows][V]); CUDA tensor, or a pinned
+        CPU tensor, which is copied into a device staging buffer on the same stream first."""
         import torch
-        if logits.dim() != 3 or logits.dtype != torch.float32:
-            raise ValueError("logits must be fp32 [batch][rows][ld]")
+        if logits.dim() != 3 or logits.dtype not in (torch.float32, torch.bfloat16):
+            raise ValueError("logits must be fp32 or bf16 [batch][rows][ld]")
         if logits.stride(2) != 1 or logits.stride(0) != logits.stride(1) * logits.shape[1]:
             raise ValueError("logits must be row-major [batch][rows][ld] (unit column stride)")
         if not logits.is_cuda:
-            n = logits.numel()
+            n = logits.numel() * logits.element_size()
             if self._staging is None or self._staging.numel() < n:
-                self._staging = torch.empty(n, dtype=torch.float32, device=self.device)
-            dev = self._staging[:n].view(logits.shape)
+                self._staging = torch.empty(n, dtype=torch.uint8, device=self.device)
+            dev = self._staging[:n].view(logits.dtype).view(logits.shape)
             s = stream if stream is not None else torch.cuda.current_stream()
             with torch.cuda.stream(s):
                 dev.copy_(logits, non_blocking=True)
             logits = dev
         b, rows = logits.shape[0], logits.shape[1]
-        xgr_beam_step(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), rows, logits.stride(1),
-                      self._stream(stream))
+        dt = XGR_DTYPE_BF16 if logits.dtype == torch.bfloat16 else XGR_DTYPE_F32
+        xgr_beam_step_ex(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), dt, rows, logits.stride(1),
+                         self._stream(stream))
         self.batch = b
         self.t += 1
 

@@ -249,8 +249,8 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
 
 // Validates a step's inputs and fills the launch arguments (shared by xgr_beam_step and the
 // codebook-shard phases). `what` names the caller in error messages.
-static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
-                            const char* what, StepArgs& a, int& rows_live) {
+static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype, int32_t rows,
+                            int64_t ld, const char* what, StepArgs& a, int& rows_live) {
   if (!ctx) return fail(XGR_ERR_INVALID_ARG, "%s: ctx is NULL", what);
   if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "%s: mask_build has not run", what);
   if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "%s: already %d steps; call finalize", what, ctx->nd);
@@ -264,12 +264,16 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const float* logits, in
   if (rows < need_rows) return fail(XGR_ERR_INVALID_ARG, "%s (step %d): rows %d < %d", what, t, rows, need_rows);
   const int Vl = ctx->V / ctx->cfg.nranks;
   if (ld < Vl) return fail(XGR_ERR_INVALID_ARG, "%s: ld %lld < %d columns", what, (long long)ld, Vl);
-  if ((reinterpret_cast<uintptr_t>(logits) & 15u) || (ld & 3))
-    return fail(XGR_ERR_ALIGNMENT, "%s: logits must be 16-byte aligned and ld %% 4 == 0", what);
+  if (dtype != XGR_DTYPE_F32 && dtype != XGR_DTYPE_BF16)
+    return fail(XGR_ERR_UNSUPPORTED, "%s: logits dtype %d (XGR_DTYPE_F32 or XGR_DTYPE_BF16)", what, dtype);
+  const int per16 = dtype == XGR_DTYPE_BF16 ? 8 : 4;   // elements per 16 bytes
+  if ((reinterpret_cast<uintptr_t>(logits) & 15u) || (ld % per16))
+    return fail(XGR_ERR_ALIGNMENT, "%s: logits must be 16-byte aligned and ld %% %d == 0", what, per16);
 
   memset(&a, 0, sizeof(a));
   a.trie = trie_dev(ctx->trie);
   a.logits = logits;
+  a.dtype = dtype;
   a.req_stride = (int64_t)rows * ld;
   a.ld = ld;
   a.t = t;
@@ -320,9 +324,14 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const float* logits, in
 
 xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
                          void* stream) {
+  return xgr_beam_step_ex(ctx, batch, logits, XGR_DTYPE_F32, rows, ld, stream);
+}
+
+xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype, int32_t rows,
+                            int64_t ld, void* stream) {
   StepArgs a;
   int rows_live = 0;
-  xgr_status st = step_args(ctx, batch, logits, rows, ld, "step", a, rows_live);
+  xgr_status st = step_args(ctx, batch, logits, dtype, rows, ld, "step", a, rows_live);
   if (st != XGR_OK) return st;
   if (ctx->cfg.nranks > 1)
     return fail(XGR_ERR_SEQUENCE, "step: codebook-sharded ctx: use xgr_shard_stats/select/merge");
@@ -334,6 +343,8 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
       !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sparse_keys <= kSparseCap;
   if (!sparse_route && ctx->V > 16384)
     return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 needs the codebook shard (nranks > 1)");
+  if (!sparse_route && dtype == XGR_DTYPE_BF16 && ctx->V % 128 != 0)
+    return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need V %% 128 == 0");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (!ctx->ev.empty() && !sparse_route && ctx->ev_head - ctx->ev_tail < kTimingRing) {
@@ -359,7 +370,7 @@ xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int
                            void* stream, const float** stats) {
   StepArgs a;
   int rows_live = 0;
-  xgr_status st = step_args(ctx, batch, logits, rows, ld, "shard_stats", a, rows_live);
+  xgr_status st = step_args(ctx, batch, logits, XGR_DTYPE_F32, rows, ld, "shard_stats", a, rows_live);
   if (st != XGR_OK) return st;
   if (ctx->shard_phase != 0) return fail(XGR_ERR_SEQUENCE, "shard_stats: previous step not merged");
   if (!stats) return fail(XGR_ERR_INVALID_ARG, "shard_stats: stats is NULL");

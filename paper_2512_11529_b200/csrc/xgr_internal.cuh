@@ -1,6 +1,7 @@
 // Internal device structures and helpers of the xBeam library (not part of the ABI).
 // Everything here is product code: it shares nothing with oracle/.
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -41,7 +42,8 @@ struct TrieDev {
 // ---- one step's arguments (passed as a __grid_constant__ kernel parameter) ------------------
 struct StepArgs {
   TrieDev trie;
-  const float* logits;
+  const void* logits;   // [batch][rows][ld] of fp32 or bf16 (dtype)
+  int32_t dtype;        // XGR_DTYPE_F32 / XGR_DTYPE_BF16
   int64_t req_stride;   // rows * ld (floats)
   int64_t ld;
   int32_t t;            // 1-based step
@@ -127,6 +129,28 @@ __device__ __forceinline__ float o2f(uint32_t o) {
 }
 __device__ __forceinline__ float theta_value(uint32_t th) {
   return th == 0u ? -INFINITY : o2f(th);
+}
+
+// Logit element loads: fp32 as is; bf16 widened exactly to fp32 (R19 / NEXT f1).
+__device__ __forceinline__ float ldx(const float* p) { return *p; }
+__device__ __forceinline__ float ldx(const __nv_bfloat16* p) {
+  return __uint_as_float((uint32_t)*reinterpret_cast<const uint16_t*>(p) << 16);
+}
+template <typename TI>
+__device__ __forceinline__ void unpack_chunk(const uint4 r, float* v) {
+  if constexpr (sizeof(TI) == 4) {
+    v[0] = __uint_as_float(r.x);
+    v[1] = __uint_as_float(r.y);
+    v[2] = __uint_as_float(r.z);
+    v[3] = __uint_as_float(r.w);
+  } else {   // 8 bf16: the low half of each word is the lower-index token
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[2 * k] = __uint_as_float(w[k] << 16);
+      v[2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
+  }
 }
 
 // 64-bit candidate key: one unsigned compare = (score desc, flat index asc) (R4).

@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(T) k_theta(const __grid_constant__ StepArgs a)
   if (slot < 0) return;
   const uint32_t nchild = L.first_child[node + 1] - L.first_child[node];
   if (nchild < (uint32_t)a.BW) return;
-  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const float* row = static_cast<const float*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
   DenseRow<T, VPT> r;
   dense_row_compute<T, VPT>(row, L.bitmap + (size_t)slot * a.trie.W, a.trie.V, a.trie.W, s_bm,
                             s_red, s_red2, r);
@@ -738,7 +738,7 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
     return;
   }
   if (tid == 0) count_add(a, XGR_CNT_ROWS_READ, 1);
-  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const float* row = static_cast<const float*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   if (slot < 0) {
@@ -811,11 +811,11 @@ __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) 
 // to keys >= theta. Keys are recomputed with the same formula and the lse stored by k_main, so
 // they are bitwise the keys k_main would have emitted. Rare path (adversarial ties/logits).
 // ---------------------------------------------------------------------------------------------
-template <int T, typename F>
+template <int T, typename TI, typename F>
 __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, int b, float S,
                                                    float lse, uint32_t node, F&& f) {
   // this rank's columns [col0, col0 + Vl) (the whole row unless codebook-sharded)
-  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
@@ -825,11 +825,10 @@ __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, i
     for (int q = threadIdx.x; 4 * q < Vl; q += T) {
       uint32_t nb = (bm[q >> 3] >> ((q & 7) * 4)) & 0xFu;
       if (!nb) continue;
-      float4 x = ld_stream4(row + 4 * q);
-      float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        if ((nb >> j) & 1u) f(make_key(cand_score(S, xs[j], lse), fbase + (uint32_t)a.col0 + 4u * q + j));
+        if ((nb >> j) & 1u)
+          f(make_key(cand_score(S, ldx(row + 4 * q + j), lse), fbase + (uint32_t)a.col0 + 4u * q + j));
     }
   } else {
     const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
@@ -837,12 +836,12 @@ __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, i
     for (uint32_t k = fc + threadIdx.x; k < fe; k += T) {
       uint32_t v = lab[k];
       if (v < (uint32_t)a.col0 || v >= (uint32_t)(a.col0 + a.Vl)) continue;
-      f(make_key(cand_score(S, row[v - a.col0], lse), fbase + v));
+      f(make_key(cand_score(S, ldx(row + (v - a.col0)), lse), fbase + v));
     }
   }
 }
 
-template <int T>
+template <int T, typename TI>
 __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uint64_t* s_out,
                                 uint32_t* s_hist, uint32_t* s_m32, const ParentInfo& s_pi) {
   const int tid = threadIdx.x;
@@ -861,7 +860,7 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
       row_state(a, req, b, S, node);
       const float lse = a.lse[(size_t)req * a.BW + b];
       if (S < th || lse != lse) continue;
-      for_each_candidate<T>(a, req, b, S, lse, node, [&](uint64_t key) {
+      for_each_candidate<T, TI>(a, req, b, S, lse, node, [&](uint64_t key) {
         if (key >= klo && (key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 0xFFu], 1u);
       });
     }
@@ -892,7 +891,7 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
     row_state(a, req, b, S, node);
     const float lse = a.lse[(size_t)req * a.BW + b];
     if (S < th || lse != lse) continue;
-    for_each_candidate<T>(a, req, b, S, lse, node, [&](uint64_t key) {
+    for_each_candidate<T, TI>(a, req, b, S, lse, node, [&](uint64_t key) {
       if (key >= thr && key >= klo) {
         uint32_t p = atomicAdd(&s_m32[2], 1u);
         if (p < (uint32_t)k) s_sel[p] = key;
@@ -908,7 +907,7 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
 // ---------------------------------------------------------------------------------------------
 // k_select: per request, top-BW of the survivors (a4) and commit (a5).
 // ---------------------------------------------------------------------------------------------
-template <int T>
+template <int T, typename TI = float>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
   uint64_t* s_cand = s_keys + a.cap;
@@ -934,7 +933,7 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
     }
     prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
     __syncthreads();
-    fallback_select<T>(a, req, s_sel, s_out, s_sc.hist, s_sc.m32, s_pi);
+    fallback_select<T, TI>(a, req, s_sel, s_out, s_sc.hist, s_sc.m32, s_pi);
     return;
   }
   const int k = min((int)n, a.BW);
@@ -1007,7 +1006,7 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
 // rows with <= 16 children (all rows' dependent load chains node -> first_child -> labels ->
 // logits run concurrently), and one warp per row for the rare larger rows.
 // ---------------------------------------------------------------------------------------------
-template <int T, bool ROOT>
+template <int T, bool ROOT, typename TI = float>
 __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
   uint64_t* s_cand = s_dynk;
@@ -1047,7 +1046,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       float S;
       uint32_t node;
       row_state(a, req, b, S, node);
-      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
       const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
       if (fe - fc <= (uint32_t)(T * RPT)) {
         // all loads issued up front: labels, then the logits they select
@@ -1061,7 +1060,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const uint32_t q = fc + (uint32_t)(k * T + tid);
-          xv[k] = q < fe ? row[vv[k]] : -INFINITY;
+          xv[k] = q < fe ? ldx(row + vv[k]) : -INFINITY;
         }
         float tmax = -INFINITY;
 #pragma unroll
@@ -1087,11 +1086,11 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         continue;
       }
       float tmax = -INFINITY;
-      for (uint32_t k = fc + tid; k < fe; k += T) tmax = fmaxf(tmax, row[lab[k]]);
+      for (uint32_t k = fc + tid; k < fe; k += T) tmax = fmaxf(tmax, ldx(row + lab[k]));
       const float M = block_max<T>(tmax, s_red);
       float z = 0.f;
       for (uint32_t k = fc + tid; k < fe; k += T)
-        z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
+        z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[k]), M), kLog2e));
       const float Z = block_sum<T>(z, s_red2);
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
       const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
@@ -1099,7 +1098,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       const uint32_t base = s_count;
       for (uint32_t k = fc + tid; k < fe; k += T) {
         uint32_t v = lab[k];
-        s_keys[base + (k - fc)] = make_key(cand_score(S, row[v], lse), (uint32_t)b * V + v);
+        s_keys[base + (k - fc)] = make_key(cand_score(S, ldx(row + v), lse), (uint32_t)b * V + v);
       }
       __syncthreads();
       if (tid == 0) s_count = base + (fe - fc);
@@ -1122,13 +1121,13 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         s_big[atomicAdd(&s_nbig, 1u)] = b;
         continue;
       }
-      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
       uint32_t vv[kSmall];
       float xv[kSmall];
 #pragma unroll
       for (int k = 0; k < kSmall; ++k) vv[k] = k < cnt ? lab[fc + k] : 0u;
 #pragma unroll
-      for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? row[vv[k]] : -INFINITY;
+      for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? ldx(row + vv[k]) : -INFINITY;
       float M = -INFINITY;
 #pragma unroll
       for (int k = 0; k < kSmall; ++k) M = fmaxf(M, xv[k]);
@@ -1152,14 +1151,14 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       float S;
       uint32_t node;
       row_state(a, req, b, S, node);
-      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
       const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
       float tmax = -INFINITY;
-      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, row[lab[k]]);
+      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, ldx(row + lab[k]));
       const float M = warp_max(tmax);
       float z = 0.f;
       for (uint32_t k = fc + lane; k < fe; k += 32)
-        z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
+        z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[k]), M), kLog2e));
       const float Z = warp_sum(z);
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
       const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
@@ -1169,7 +1168,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       base = __shfl_sync(0xffffffffu, base, 0);
       for (uint32_t k = fc + lane; k < fe; k += 32) {
         uint32_t v = lab[k];
-        s_keys[base + (k - fc)] = make_key(cand_score(S, row[v], lse), (uint32_t)b * V + v);
+        s_keys[base + (k - fc)] = make_key(cand_score(S, ldx(row + v), lse), (uint32_t)b * V + v);
       }
     }
   }
@@ -1250,16 +1249,22 @@ __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
   const LevelDev& L = a.trie.lv[a.level];
   const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
   const int V = a.trie.V;
+  const int esz = a.dtype == XGR_DTYPE_BF16 ? 2 : 4;   // bytes per logit; a 32-B sector holds 32/esz
   if (threadIdx.x == 0) {
-    atomicAdd(out + 1, (unsigned long long)V * 4ull);
+    atomicAdd(out + 1, (unsigned long long)V * (unsigned long long)esz);
     atomicAdd(out + 2, (unsigned long long)(fe - fc));
   }
   if (S < thstar) return;  // a row the method need not read
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   unsigned long long bytes = 0;
   if (slot >= 0) {
-    const uint8_t* bm = reinterpret_cast<const uint8_t*>(L.bitmap + (size_t)slot * a.trie.W);
-    for (int s = threadIdx.x; s < (V + 7) / 8; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+    if (esz == 4) {   // 8 tokens per sector: one bitmap byte
+      const uint8_t* bm = reinterpret_cast<const uint8_t*>(L.bitmap + (size_t)slot * a.trie.W);
+      for (int s = threadIdx.x; s < (V + 7) / 8; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+    } else {          // 16 tokens per sector: one bitmap half-word
+      const uint16_t* bm = reinterpret_cast<const uint16_t*>(L.bitmap + (size_t)slot * a.trie.W);
+      for (int s = threadIdx.x; s < (V + 15) / 16; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+    }
     if (threadIdx.x == 0) {
       uint32_t old = atomicOr(touched + (slot >> 5), 1u << (slot & 31));
       if (!((old >> (slot & 31)) & 1u)) bytes += (unsigned long long)((V + 7) / 8);
@@ -1268,7 +1273,7 @@ __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
   } else {
     const uint16_t* lab = a.trie.lv[a.level + 1].label;
     for (uint32_t k2 = fc + threadIdx.x; k2 < fe; k2 += blockDim.x)
-      if (k2 == fc || (lab[k2] >> 3) != (lab[k2 - 1] >> 3)) bytes += 32;
+      if (k2 == fc || (lab[k2] * esz) / 32 != (lab[k2 - 1] * esz) / 32) bytes += 32;
     if (threadIdx.x == 0) bytes += 4 + 2ull * (fe - fc) + 16;
   }
   bytes = __reduce_add_sync(0xffffffffu, (unsigned)bytes);
@@ -1301,14 +1306,16 @@ cudaError_t configure_stream_kernels();
 cudaError_t configure_kernels(int cap) {
   cudaError_t e = configure_stream_kernels();
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((cap + 2 * kMaxBW) * sizeof(uint64_t)));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_sparse<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)((kSparseCap + 2 * kMaxBW) * sizeof(uint64_t)));
-  if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_sparse<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)((kSparseCap + 2 * kMaxBW) * sizeof(uint64_t)));
+  const int sel = (int)((cap + 2 * kMaxBW) * sizeof(uint64_t));
+  const int spk = (int)((kSparseCap + 2 * kMaxBW) * sizeof(uint64_t));
+  if ((e = cudaFuncSetAttribute(k_select<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel)) ||
+      (e = cudaFuncSetAttribute(k_select<512, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, sel)) ||
+      (e = cudaFuncSetAttribute(k_sparse<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)) ||
+      (e = cudaFuncSetAttribute(k_sparse<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)) ||
+      (e = cudaFuncSetAttribute(k_sparse<512, true, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)))
+    return e;
+  return cudaFuncSetAttribute(k_sparse<512, false, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              spk);
 }
 
 bool stream_supported(int V);
@@ -1318,14 +1325,21 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
 cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int sparse_keys,
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
+  const bool bf16 = a.dtype == XGR_DTYPE_BF16;
   if (sparse_route) {
     size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
-    if (rows == 1) k_sparse<512, true><<<a.batch, 512, smem, s>>>(a);
-    else k_sparse<512, false><<<a.batch, 512, smem, s>>>(a);
+    if (bf16) {
+      if (rows == 1) k_sparse<512, true, __nv_bfloat16><<<a.batch, 512, smem, s>>>(a);
+      else k_sparse<512, false, __nv_bfloat16><<<a.batch, 512, smem, s>>>(a);
+    } else {
+      if (rows == 1) k_sparse<512, true><<<a.batch, 512, smem, s>>>(a);
+      else k_sparse<512, false><<<a.batch, 512, smem, s>>>(a);
+    }
     ++*launches;
     return cudaGetLastError();
   }
   const int V = a.trie.V;
+  if (bf16 && !stream_supported(V)) return cudaErrorNotSupported;   // the API checks this first
   if (stream_supported(V)) {
     e = launch_stream(a, rows, s, ev0, ev1, launches);   // k_seed resets theta/count/ovf
   } else if ((e = cudaMemsetAsync(a.theta, 0, (size_t)a.batch * 4, s)) != cudaSuccess ||
@@ -1338,7 +1352,9 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   else if (V <= 16384) e = launch_dense<512, 8>(a, rows, s, ev0, ev1, launches);
   else return cudaErrorNotSupported;
   if (e != cudaSuccess) return e;
-  k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
+  const size_t sel = ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t);
+  if (bf16) k_select<512, __nv_bfloat16><<<a.batch, 512, sel, s>>>(a);
+  else k_select<512><<<a.batch, 512, sel, s>>>(a);
   *launches += 1;
   return cudaGetLastError();
 }

@@ -54,6 +54,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// The same wait with a suspend-time hint: the thread sleeps in hardware until the phase completes
+// (or the hint expires) instead of re-polling (NANOSLEEP.SYNCS); for the producer warp, whose
+// empty-slot waits otherwise spin for tens of polls per row and steal the consumers' issue slots.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                          uint64_t policy) {
   asm volatile(
@@ -202,7 +214,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
       const uint64_t pol = policy_evict_first();
       for (int r = 0; r < R0; ++r) {
         if (!r_kind[r]) continue;
-        const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
+        const float* row = static_cast<const float*>(a.logits) + (size_t)req * a.req_stride + (size_t)r * a.ld;
         bulk_g2s(s_row + (size_t)r * 32 * CTR, row, rb, &bar, pol);
         bulk_g2s(s_msk + (size_t)r * CTR, L.bitmap + (size_t)r_slot[r] * W + (a.col0 >> 5), mb, &bar, pol);
       }
@@ -476,8 +488,10 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 // count reaches BW: theta = S_0 - (bin + 1) / 128 - margin has >= BW candidates above it, so it is
 // <= the request's BW-th best score. The seed rows are then streamed like any other row.
 // ------------------------------------------------------------------------------------------
-template <int T, int VPT>
+template <int T, int NCH, typename TI = float>
 __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
+  constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk
+  constexpr int VPT = NCH * CH / 4;          // x[] holds 4 * VPT = NCH * CH tokens per thread
   constexpr int NW = T / 32;
   __shared__ float2 part[NW];
   __shared__ float s_tau[NW];
@@ -485,16 +499,16 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   const int req = blockIdx.x, r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   // The row (always in bounds: r < rows) and the beam state are loaded up front and together;
   // only the dense slot and then its bitmap depend on earlier loads.
-  const float* row = a.logits + (size_t)req * a.req_stride + (size_t)r * a.ld;
+  const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)r * a.ld;
   const int Vl = a.Vl;
-  float4 v[VPT];
+  uint4 v[NCH];
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < NCH; ++i) {
     const int q = i * T + tid;
-    v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (4 * q < Vl)
-      asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                   : "=f"(v[i].x), "=f"(v[i].y), "=f"(v[i].z), "=f"(v[i].w) : "l"(row + 4 * q));
+    v[i] = make_uint4(0u, 0u, 0u, 0u);
+    if (CH * q < Vl)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w) : "l"(row + CH * q));
   }
   const int nl = nlive_of(a, req);
   float S;
@@ -508,13 +522,13 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W + (a.col0 >> 5);
   float x[4 * VPT];
 #pragma unroll
-  for (int i = 0; i < VPT; ++i) {
+  for (int i = 0; i < NCH; ++i) {
     const int q = i * T + tid;
-    const uint32_t nb = (4 * q < Vl) ? (__ldg(bm + (q >> 3)) >> (4 * (q & 7))) & 0xFu : 0u;
-    x[4 * i] = (nb & 1u) ? v[i].x : -INFINITY;
-    x[4 * i + 1] = (nb & 2u) ? v[i].y : -INFINITY;
-    x[4 * i + 2] = (nb & 4u) ? v[i].z : -INFINITY;
-    x[4 * i + 3] = (nb & 8u) ? v[i].w : -INFINITY;
+    const uint32_t nb = (CH * q < Vl) ? (__ldg(bm + ((CH * q) >> 5)) >> ((CH * q) & 31)) & ((1u << CH) - 1u) : 0u;
+    float f[CH];
+    unpack_chunk<TI>(v[i], f);
+#pragma unroll
+    for (int j = 0; j < CH; ++j) x[CH * i + j] = ((nb >> j) & 1u) ? f[j] : -INFINITY;
   }
   float lse;
   if (a.gstats) {   // codebook shard: the global lse from all ranks' stats
@@ -656,17 +670,19 @@ __device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
   }
 }
 
-template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal>
+template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float>
 __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   constexpr int GT = 256;          // consumer threads per group
   constexpr int VT = GT * EPT;     // tokens per stage row
   constexpr int MW = VT / 32;      // mask words per stage
-  constexpr int NF4 = EPT / 4;     // float4 per thread
+  constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk (4 fp32, 8 bf16)
+  constexpr int NCH = EPT / CH;               // chunks per thread
+  constexpr uint32_t CHM = (1u << CH) - 1u;   // a chunk's mask bits
   constexpr int NC = GT * G;       // consumer threads
-  extern __shared__ __align__(128) float s_dyn[];
-  float* s_row = s_dyn;                                             // [NS][VT]
-  uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dyn + NS * VT);  // [NS][MW]
+  extern __shared__ __align__(128) unsigned char s_dynb[];
+  TI* s_row = reinterpret_cast<TI*>(s_dynb);                                         // [NS][VT]
+  uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dynb + (size_t)NS * VT * sizeof(TI));  // [NS][MW]
   __shared__ __align__(8) uint64_t full[NS], empty[NS];
   __shared__ Desc desc[NS];
   __shared__ float s_th[NS];
@@ -768,7 +784,10 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         const float jlse = __shfl_sync(0xffffffffu, m0.lse, j);
         if (lane == 0) {
           const int st = kj % NS;
-          if (kj >= NS) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
+          if (kj >= NS) {
+            if (a.dbg & 4096) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
+            else mbar_wait_sleep(&empty[st], ((kj / NS) - 1) & 1);
+          }
           Desc d;
           d.req = jreq;
           d.b = jb;
@@ -780,8 +799,8 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
           desc[st] = d;
           s_th[st] = jth;
           if (jkind == 1) {
-            const float* row = a.logits + (size_t)jreq * a.req_stride + (size_t)jb * a.ld;
-            const uint32_t rb = (uint32_t)a.Vl * 4u, mb = (uint32_t)(a.Vl >> 5) * 4u;
+            const TI* row = static_cast<const TI*>(a.logits) + (size_t)jreq * a.req_stride + (size_t)jb * a.ld;
+            const uint32_t rb = (uint32_t)a.Vl * (uint32_t)sizeof(TI), mb = (uint32_t)(a.Vl >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
             bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
             // a dense node's bitmap is shared by every row whose beam sits on it: keep it in L2
@@ -857,7 +876,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (d.kind == 0) continue;
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
-      const float* row = a.logits + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
       uint32_t fc = L.first_child[d.node], fe = L.first_child[d.node + 1];
       if (a.Vl != V) {   // codebook shard: the children whose token lies in this rank's columns
         uint32_t lo = fc, hi = fe;
@@ -881,11 +900,11 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         if (lt == 0) a.lse[(size_t)req * BW + b] = lse;
       } else {
         float tm = -INFINITY;
-        for (uint32_t q = fc + lt; q < fe; q += GT) tm = fmaxf(tm, row[lab[q]]);
+        for (uint32_t q = fc + lt; q < fe; q += GT) tm = fmaxf(tm, ldx(row + lab[q]));
         M = gmax(tm);
         float z = 0.f;
         for (uint32_t q = fc + lt; q < fe; q += GT)
-          z += ex2f(__fmul_rn(__fsub_rn(row[lab[q]], M), kLog2eS));
+          z += ex2f(__fmul_rn(__fsub_rn(ldx(row + lab[q]), M), kLog2eS));
         const float Z = gsum(z);
         if (MODE == kModeStats) {   // local (m, Z); an empty slice is (-inf, 0)
           if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
@@ -908,7 +927,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         float c = -INFINITY;
         if (q < fe) {
           v = lab[q];
-          c = cand_score(S, row[v], lse);
+          c = cand_score(S, ldx(row + v), lse);
         }
         const bool take = q < fe && c >= th;
         if (__any_sync(0xffffffffu, take)) {
@@ -919,21 +938,21 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       continue;
     }
 
-    // ---- dense row: stage -> registers. Thread lt owns float4 q = i*GT + lt (i < NF4): 16-byte
-    // consecutive per lane, conflict-free, compile-time offsets; its mask nibble is bits
-    // 4*(lt & 7) .. +3 of word q / 8 = i*GT/8 + lt/8.
-    const float* srow = s_row + (size_t)st * VT + 4 * lt;
-    const uint32_t* smsk = s_msk + (size_t)st * MW + (lt >> 3);
-    const int nsh = 4 * (lt & 7);
+    // ---- dense row: stage -> registers. Thread lt owns the 16-byte chunks q = i*GT + lt
+    // (i < NCH; CH tokens each): consecutive per lane, conflict-free, compile-time offsets; its
+    // mask bits are CH*(lt % (32/CH)) .. +CH-1 of word q*CH/32 = i*GT*CH/32 + lt/(32/CH).
+    const TI* srow = s_row + (size_t)st * VT + CH * lt;
+    const uint32_t* smsk = s_msk + (size_t)st * MW + (lt / (32 / CH));
+    const int nsh = CH * (lt & (32 / CH - 1));
     float x[EPT];
 #pragma unroll
-    for (int i = 0; i < NF4; ++i) {
-      const float4 v4 = *reinterpret_cast<const float4*>(srow + i * GT * 4);
-      const uint32_t nb = smsk[i * (GT / 8)] >> nsh;
-      x[4 * i] = (nb & 1u) ? v4.x : -INFINITY;
-      x[4 * i + 1] = (nb & 2u) ? v4.y : -INFINITY;
-      x[4 * i + 2] = (nb & 4u) ? v4.z : -INFINITY;
-      x[4 * i + 3] = (nb & 8u) ? v4.w : -INFINITY;
+    for (int i = 0; i < NCH; ++i) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(srow + i * GT * CH);
+      const uint32_t nb = smsk[i * (GT * CH / 32)] >> nsh;
+      float v[CH];
+      unpack_chunk<TI>(raw, v);
+#pragma unroll
+      for (int j = 0; j < CH; ++j) x[CH * i + j] = ((nb >> j) & 1u) ? v[j] : -INFINITY;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -1003,7 +1022,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       const float xthr = (th - S) + lse - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse));
       if (tmax >= xthr) {
 #pragma unroll
-        for (int i = 0; i < NF4; ++i) {
+        for (int i = 0; i < EPT / 4; ++i) {   // gated by groups of 4
           const float m4 = fmaxf(fmaxf(x[4 * i], x[4 * i + 1]), fmaxf(x[4 * i + 2], x[4 * i + 3]));
           if (m4 >= xthr) {
 #pragma unroll
@@ -1017,12 +1036,12 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
       // included, is a candidate; legality re-read from the node's bitmap in global memory
-      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (a.col0 >> 5) + (lt >> 3);
+      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (a.col0 >> 5) + (lt / (32 / CH));
 #pragma unroll
-      for (int i = 0; i < NF4; ++i) {
+      for (int i = 0; i < NCH; ++i) {
         const uint32_t q4 = (uint32_t)(i * GT + lt);
-        const uint32_t nb = (4 * q4 < (uint32_t)a.Vl) ? ((__ldg(gm + i * (GT / 8)) >> nsh) & 0xFu) : 0u;
-        mine |= (uint64_t)nb << (4 * i);
+        const uint32_t nb = (CH * q4 < (uint32_t)a.Vl) ? ((__ldg(gm + i * (GT * CH / 32)) >> nsh) & CHM) : 0u;
+        mine |= (uint64_t)nb << (CH * i);
       }
     }
     const int ns = __popcll(mine);
@@ -1036,7 +1055,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           if ((mine >> e) & 1ull) {
-            const uint32_t v = 4u * (uint32_t)((e >> 2) * GT + lt) + (e & 3);
+            const uint32_t v = (uint32_t)CH * (uint32_t)((e / CH) * GT + lt) + (uint32_t)(e % CH);
             if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, x[e], lse), fbase + v);
             ++pos;
           }
@@ -1044,14 +1063,14 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       } else {
         int q = 0;
 #pragma unroll
-        for (int i = 0; i < NF4; ++i) {
-          const uint32_t nb = (uint32_t)(mine >> (4 * i)) & 0xFu;
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t nb = (uint32_t)(mine >> (CH * i)) & CHM;
           if (nb) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < CH; ++j) {
               if ((nb >> j) & 1u) {
-                const uint32_t v = 4u * (uint32_t)(i * GT + lt) + j;
-                const uint64_t key = make_key(cand_score(S, x[4 * i + j], lse), fbase + v);
+                const uint32_t v = (uint32_t)CH * (uint32_t)(i * GT + lt) + j;
+                const uint64_t key = make_key(cand_score(S, x[CH * i + j], lse), fbase + v);
                 if (q == 0) pend_k0 = key; else pend_k1 = key;
                 ++q;
               }
@@ -1079,9 +1098,9 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
   flush();
 }
 
-template <int EPT, int NS>
+template <int EPT, int NS, typename TI = float>
 static size_t stream_smem() {
-  return (size_t)NS * (256 * EPT * sizeof(float) + 256 * EPT / 8);
+  return (size_t)NS * (256 * EPT * sizeof(TI) + 256 * EPT / 8);
 }
 
 static int g_num_sms = 0;
@@ -1110,6 +1129,10 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeStats>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeShardEmit>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 2>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 4, 3, kModeNormal, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) != cudaSuccess)
+    return e;
+  if ((e = opt_in(k_stream<64, 1, 3, 2, kModeNormal, __nv_bfloat16>, stream_smem<64, 3, __nv_bfloat16>())) != cudaSuccess)
+    return e;
   if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
   if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
@@ -1141,6 +1164,26 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int total = a.batch * rows;
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
+  if (a.dtype == XGR_DTYPE_BF16) {   // NEXT f1: bf16 rows (half the bytes), histogram seed
+    using bf = __nv_bfloat16;
+    const int r0 = std::min(a.theta_rows, rows);
+    if (r0 > 0) {
+      if (a.trie.V <= 8192) k_seed_hist<256, 4, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      else k_seed_hist<256, 8, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      ++*launches;
+    }
+    k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+    if (ev0) cudaEventRecord(ev0, s);
+    if (a.trie.V <= 8192)
+      k_stream<32, 1, 4, 3, kModeNormal, bf><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s>>>(
+          a, total, 0);
+    else
+      k_stream<64, 1, 3, 2, kModeNormal, bf><<<std::min(total, 2 * sms), 256 + 32, stream_smem<64, 3, bf>(), s>>>(
+          a, total, 0);
+    if (ev1) cudaEventRecord(ev1, s);
+    *launches += 2;
+    return cudaGetLastError();
+  }
   if (a.trie.V <= 8192) {
     int seeded = g_seed_rows == 2 ? 2 : 4;
     if (g_seed_mode == 1) {   // histogram seed over rows 0..R0-1; every row is then streamed

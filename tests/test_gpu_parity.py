@@ -45,7 +45,7 @@ def run_checked(bs, voc, logits_steps, bw, check_reqs, logits_fn=None):
         sc = v["score"].cpu().numpy().copy()
         nl = v["n_live"].cpu().numpy().copy()
         for r in check_reqs:
-            lr = lg[r].cpu().numpy()
+            lr = lg[r].float().cpu().numpy()   # bf16 widened exactly (R19 / NEXT f1)
             res = compare_step(voc, states[r], lr, bw, par[r], tok[r], sc[r], nl[r],
                                where=f"req {r} step {t + 1}")
             stats[res] += 1

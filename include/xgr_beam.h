@@ -228,6 +228,21 @@ int64_t xgr_beam_launch_count(const xgr_ctx* ctx);
  * XGR_CFG_TIMING. Writes min(recorded, cap) entries and *n; synchronises on the events. */
 xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t cap, int32_t* n);
 
+/* ---- KV-cache reorder after a step (section 5.1, Fig. 6:
+ * the unshared per-beam cache "updates block contents based on beam indices").
+ * For every request r < n_req, panel p < n_panel (e.g. a layer's K or V panel) and slot j < bw
+ * with s = src[r*src_ld + j] >= 0: new row (r, p, j) = old row (r, p, s), in place. Row (r, p, j)
+ * is the row_bytes bytes at cache + r*req_stride + p*panel_stride + j*beam_stride (DEVICE memory;
+ * cache, row_bytes and every stride 16-byte aligned; beam_stride >= row_bytes). src: DEVICE int32,
+ * e.g. a step's parent[] (xgr_beam_view / xgr_beam_history); s < 0 (dead slot) and s == j leave
+ * the row untouched. Any map is allowed, not only SPEC's monotone plans: rows are moved in column
+ * tiles staged in shared memory, so no row is overwritten before it has been read, without an
+ * auxiliary copy of the cache. bw 1..1024. Enqueues only (graph-capturable); no ctx needed.
+ * Errors: XGR_ERR_INVALID_ARG (sizes, NULL), XGR_ERR_ALIGNMENT, XGR_ERR_CUDA. */
+xgr_status xgr_kv_reorder(void* cache, int32_t n_req, int32_t n_panel, int32_t bw, int64_t row_bytes,
+                          int64_t beam_stride, int64_t panel_stride, int64_t req_stride,
+                          const int32_t* src, int32_t src_ld, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,6 +14,7 @@ from .binding import (  # noqa: F401
     XGR_CFG_TIMING,
     XGR_DTYPE_BF16,
     XGR_DTYPE_F32,
+    kv_reorder,
     lib,
     LIB_PATH,
 )

@@ -32,7 +32,7 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_step_ex
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
            "xgr_beam_kernel_times", "xgr_beam_outputs", "xgr_shard_stats", "xgr_shard_select",
-           "xgr_shard_merge"]
+           "xgr_shard_merge", "xgr_kv_reorder"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -77,6 +77,7 @@ def _load():
         "xgr_shard_stats": [VP, I32, VP, I32, I64, VP, P(VP)],
         "xgr_shard_select": [VP, VP, VP, P(VP), P(VP)],
         "xgr_shard_merge": [VP, VP, VP, VP],
+        "xgr_kv_reorder": [VP, I32, I32, I32, I64, I64, I64, I64, VP, I32, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -370,6 +371,24 @@ class BeamSearch:
         _check(lib.xgr_beam_account(self.ctx, ctypes.byref(a), ctypes.byref(f), ctypes.byref(lg),
                                     self._stream()))
         return {"alg_bytes": a.value, "full_bytes": f.value, "legal": lg.value}
+
+
+def kv_reorder(cache, src, stream=None):
+    """In-place KV-cache reorder after a step (xgr_kv_reorder):
+    cache[r, p, j, :] <- cache[r, p, src[r, j], :] for src >= 0 and src != j.
+    cache: CUDA tensor [n_req][n_panel][bw][E] (last dim contiguous, rows 16-byte multiples);
+    src: CUDA int32 [n_req][>= bw], e.g. BeamSearch.view()["parent"]."""
+    import torch
+    if cache.dim() != 4 or cache.stride(3) != 1:
+        raise ValueError("cache must be [n_req][n_panel][bw][E] with a contiguous last dim")
+    if src.dtype != torch.int32 or src.dim() != 2 or src.stride(1) != 1:
+        raise ValueError("src must be int32 [n_req][>= bw] with unit column stride")
+    es = cache.element_size()
+    n_req, n_panel, bw, e = cache.shape
+    st = torch.cuda.current_stream() if stream is None else stream
+    _check(lib.xgr_kv_reorder(ctypes.c_void_p(cache.data_ptr()), n_req, n_panel, bw, e * es,
+                              cache.stride(2) * es, cache.stride(1) * es, cache.stride(0) * es,
+                              ctypes.c_void_p(src.data_ptr()), src.stride(0), ctypes.c_void_p(st.cuda_stream)))
 
 
 class ShardedBeamSearch:

@@ -607,3 +607,28 @@ xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t
 }
 
 }  // extern "C"
+
+// ---- KV-cache reorder (NEXT f2) -------------------------------------------------------------------
+namespace xgr {
+cudaError_t launch_kv_reorder(void* cache, int n_req, int n_panel, int bw, int64_t row_bytes,
+                              int64_t beam_stride, int64_t panel_stride, int64_t req_stride,
+                              const int32_t* src, int src_ld, cudaStream_t s);
+}
+
+extern "C" xgr_status xgr_kv_reorder(void* cache, int32_t n_req, int32_t n_panel, int32_t bw, int64_t row_bytes,
+                                     int64_t beam_stride, int64_t panel_stride, int64_t req_stride,
+                                     const int32_t* src, int32_t src_ld, void* stream) {
+  if (n_req < 0 || n_panel < 0 || bw < 1 || bw > kMaxBW || row_bytes < 0 || src_ld < bw)
+    return fail(XGR_ERR_INVALID_ARG, "kv_reorder: n_req %d n_panel %d bw %d row_bytes %lld src_ld %d", n_req,
+                n_panel, bw, (long long)row_bytes, src_ld);
+  if (n_req == 0 || n_panel == 0 || row_bytes == 0) return XGR_OK;
+  if (!cache || !src) return fail(XGR_ERR_INVALID_ARG, "kv_reorder: NULL cache or src");
+  if (n_req > 65535 || n_panel > 65535) return fail(XGR_ERR_INVALID_ARG, "kv_reorder: n_req, n_panel <= 65535");
+  if ((reinterpret_cast<uintptr_t>(cache) & 15u) || (row_bytes & 15) || (beam_stride & 15) ||
+      (panel_stride & 15) || (req_stride & 15))
+    return fail(XGR_ERR_ALIGNMENT, "kv_reorder: cache, row_bytes and strides must be 16-byte multiples");
+  if (beam_stride < row_bytes) return fail(XGR_ERR_INVALID_ARG, "kv_reorder: beam_stride < row_bytes");
+  ACK(xgr::launch_kv_reorder(cache, n_req, n_panel, bw, row_bytes, beam_stride, panel_stride, req_stride, src,
+                             src_ld, (cudaStream_t)stream));
+  return XGR_OK;
+}

@@ -228,6 +228,23 @@ int64_t xgr_beam_launch_count(const xgr_ctx* ctx);
  * XGR_CFG_TIMING. Writes min(recorded, cap) entries and *n; synchronises on the events. */
 xgr_status xgr_beam_kernel_times(xgr_ctx* ctx, float* ms, int32_t* step, int32_t cap, int32_t* n);
 
+/* ---- LM-head fusion at sparse steps (at the last steps each
+ * row has only a few legal tokens). Instead of logits, the step takes the decoder's final hidden
+ * states and the LM-head weight and computes only the legal tokens' logits
+ *   x[b][v] = sum_{k < d} hidden[b][k] * head[v][k]  (+ bias[v] when bias != NULL)
+ * (fp32 FMAs over bf16 inputs, a fixed order), then selects exactly as xgr_beam_step on those
+ * values. hidden: DEVICE bf16 [batch][rows][ldh], row b of request r at hidden + (r*rows + b)*ldh
+ * (ldh >= d, ldh % 8 == 0, 16-byte aligned); head: DEVICE bf16 [V][ldw] (ldw >= d, ldw % 8 == 0);
+ * bias: DEVICE fp32 [V] or NULL; d % 8 == 0. Only for a step after the root that takes the sparse
+ * route (xgr_beam_next_route == 1); otherwise XGR_ERR_UNSUPPORTED (produce logits with a GEMM and
+ * call xgr_beam_step). Enqueues only; uses a ctx-owned buffer of max_batch * 16384 floats. */
+xgr_status xgr_beam_step_head(xgr_ctx* ctx, int32_t batch, const void* hidden, int32_t rows, int64_t ldh,
+                              const void* head, int64_t ldw, const float* bias, int32_t d, void* stream);
+
+/* *sparse = 1 if the next step takes the sparse route (every request's legal candidates fit on
+ * chip: rows x max children of the level <= 16384), 0 for the dense (streaming) route. */
+xgr_status xgr_beam_next_route(const xgr_ctx* ctx, int32_t* sparse);
+
 /* ---- KV-cache reorder after a step (section 5.1, Fig. 6:
  * the unshared per-beam cache "updates block contents based on beam indices").
  * For every request r < n_req, panel p < n_panel (e.g. a layer's K or V panel) and slot j < bw

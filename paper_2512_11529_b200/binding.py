@@ -32,7 +32,7 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_step_ex
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
            "xgr_beam_kernel_times", "xgr_beam_outputs", "xgr_shard_stats", "xgr_shard_select",
-           "xgr_shard_merge", "xgr_kv_reorder"]
+           "xgr_shard_merge", "xgr_kv_reorder", "xgr_beam_step_head", "xgr_beam_next_route"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -78,6 +78,8 @@ def _load():
         "xgr_shard_select": [VP, VP, VP, P(VP), P(VP)],
         "xgr_shard_merge": [VP, VP, VP, VP],
         "xgr_kv_reorder": [VP, I32, I32, I32, I64, I64, I64, I64, VP, I32, VP],
+        "xgr_beam_step_head": [VP, I32, VP, I32, I64, VP, I64, VP, I32, VP],
+        "xgr_beam_next_route": [VP, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -240,6 +242,33 @@ class BeamSearch:
         dt = XGR_DTYPE_BF16 if logits.dtype == torch.bfloat16 else XGR_DTYPE_F32
         xgr_beam_step_ex(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), dt, rows, logits.stride(1),
                          self._stream(stream))
+        self.batch = b
+        self.t += 1
+
+    def next_is_sparse(self) -> bool:
+        """Whether the next step takes the sparse route (xgr_beam_next_route)."""
+        v = ctypes.c_int32()
+        _check(lib.xgr_beam_next_route(self.ctx, ctypes.byref(v)))
+        return bool(v.value)
+
+    def step_head(self, hidden, head, bias=None, stream=None):
+        """LM-head fusion at a sparse step (NEXT f4; xgr_beam_step_head): hidden CUDA bf16
+        [batch][rows][ldh], head CUDA bf16 [V][ldw] (only the first d = hidden.shape[2] columns
+        are used if the last dims are views), bias CUDA fp32 [V] or None."""
+        import torch
+        if hidden.dim() != 3 or hidden.dtype != torch.bfloat16 or hidden.stride(2) != 1:
+            raise ValueError("hidden must be bf16 [batch][rows][d] with unit column stride")
+        if head.dim() != 2 or head.dtype != torch.bfloat16 or head.stride(1) != 1:
+            raise ValueError("head must be bf16 [V][d] with unit column stride")
+        if bias is not None and (bias.dtype != torch.float32 or not bias.is_contiguous()):
+            raise ValueError("bias must be contiguous fp32 [V]")
+        b, rows, d = hidden.shape
+        if hidden.stride(0) != hidden.stride(1) * rows:
+            raise ValueError("hidden must be row-major [batch][rows][ldh]")
+        _check(lib.xgr_beam_step_head(self.ctx, b, ctypes.c_void_p(hidden.data_ptr()), rows, hidden.stride(1),
+                                      ctypes.c_void_p(head.data_ptr()), head.stride(0),
+                                      ctypes.c_void_p(bias.data_ptr() if bias is not None else 0), d,
+                                      self._stream(stream)))
         self.batch = b
         self.t += 1
 

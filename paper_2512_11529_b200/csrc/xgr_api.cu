@@ -43,6 +43,7 @@ struct xgr_ctx {
   int32_t** d_thist = nullptr;
   uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
   uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
+  float* head_logits = nullptr;    // [maxB][kSparseCap]: legal logits of a fused-head sparse step
   uint64_t* surv = nullptr;        // [maxB][cap]
   float* lse = nullptr;            // [maxB][BW]
   uint32_t* flags = nullptr;       // [maxB]
@@ -106,6 +107,7 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->d_thist);
   cudaFree(c->scratch);
   cudaFree(c->seed_hist);
+  cudaFree(c->head_logits);
   cudaFree(c->surv);
   cudaFree(c->lse);
   cudaFree(c->flags);
@@ -117,6 +119,12 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->shard_stats);
   cudaFree(c->shard_rec);
   cudaFree(c->shard_rec_n);
+}
+
+namespace xgr {
+cudaError_t launch_head(const StepArgs& a, const void* hidden, int64_t ldh, int64_t hreq, const void* head,
+                        int64_t ldw, const float* bias, int d, float* clog, cudaStream_t s);
+cudaError_t launch_sparse_compact(const StepArgs& a, int sparse_keys, cudaStream_t s, int* launches);
 }
 
 extern "C" {
@@ -187,6 +195,7 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->d_thist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->scratch, 3 * (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
+  if (e == cudaSuccess) e = al((void**)&x->head_logits, (size_t)x->maxB * kSparseCap * 4);
   if (e == cudaSuccess) e = cudaMemset(x->seed_hist, 0, (size_t)x->maxB * kSeedBins * 4);
   if (e == cudaSuccess) e = al((void**)&x->surv, (size_t)x->maxB * x->cap * 8);
   if (e == cudaSuccess) e = al((void**)&x->lse, nb * 4);
@@ -250,7 +259,7 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
 // Validates a step's inputs and fills the launch arguments (shared by xgr_beam_step and the
 // codebook-shard phases). `what` names the caller in error messages.
 static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype, int32_t rows,
-                            int64_t ld, const char* what, StepArgs& a, int& rows_live) {
+                            int64_t ld, const char* what, StepArgs& a, int& rows_live, int64_t min_ld = -1) {
   if (!ctx) return fail(XGR_ERR_INVALID_ARG, "%s: ctx is NULL", what);
   if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "%s: mask_build has not run", what);
   if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "%s: already %d steps; call finalize", what, ctx->nd);
@@ -263,7 +272,8 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const int need_rows = (t == 1) ? 1 : ctx->BW;
   if (rows < need_rows) return fail(XGR_ERR_INVALID_ARG, "%s (step %d): rows %d < %d", what, t, rows, need_rows);
   const int Vl = ctx->V / ctx->cfg.nranks;
-  if (ld < Vl) return fail(XGR_ERR_INVALID_ARG, "%s: ld %lld < %d columns", what, (long long)ld, Vl);
+  if (min_ld < 0) min_ld = Vl;
+  if (ld < min_ld) return fail(XGR_ERR_INVALID_ARG, "%s: ld %lld < %lld columns", what, (long long)ld, (long long)min_ld);
   if (dtype != XGR_DTYPE_F32 && dtype != XGR_DTYPE_BF16)
     return fail(XGR_ERR_UNSUPPORTED, "%s: logits dtype %d (XGR_DTYPE_F32 or XGR_DTYPE_BF16)", what, dtype);
   const int per16 = dtype == XGR_DTYPE_BF16 ? 8 : 4;   // elements per 16 bytes
@@ -360,6 +370,56 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   ctx->launches += launches;
   ctx->batch = batch;
   ctx->step = t;
+  ctx->last = a;
+  ctx->last_rows = rows_live;
+  return XGR_OK;
+}
+
+// ---- LM-head fusion at sparse steps (NEXT f4) ------------------------------------------------------
+
+static bool next_is_sparse(const xgr_ctx* ctx, int64_t* keys) {
+  const int t = ctx->step + 1;
+  const int rows_live = t == 1 ? 1 : ctx->BW;
+  const int64_t k = (int64_t)rows_live * ctx->trie.lv[t - 1].max_children;
+  if (keys) *keys = k;
+  return !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && k <= kSparseCap;
+}
+
+xgr_status xgr_beam_next_route(const xgr_ctx* ctx, int32_t* sparse) {
+  if (!ctx || !sparse) return fail(XGR_ERR_INVALID_ARG, "next_route: NULL argument");
+  if (!ctx->built) return fail(XGR_ERR_SEQUENCE, "next_route: mask_build has not run");
+  if (ctx->step >= ctx->nd) return fail(XGR_ERR_SEQUENCE, "next_route: all %d steps done", ctx->nd);
+  *sparse = next_is_sparse(ctx, nullptr) ? 1 : 0;
+  return XGR_OK;
+}
+
+xgr_status xgr_beam_step_head(xgr_ctx* ctx, int32_t batch, const void* hidden, int32_t rows, int64_t ldh,
+                              const void* head, int64_t ldw, const float* bias, int32_t d, void* stream) {
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "step_head: ctx is NULL");
+  if (d < 8 || (d & 7) || ldw < d || (ldw & 7))
+    return fail(XGR_ERR_INVALID_ARG, "step_head: d %d (a multiple of 8) and ldw %lld >= d (multiple of 8)", d,
+                (long long)ldw);
+  if (!head || (reinterpret_cast<uintptr_t>(head) & 15u))
+    return fail(XGR_ERR_ALIGNMENT, "step_head: head must be a 16-byte aligned device pointer");
+  StepArgs a;
+  int rows_live = 0;
+  xgr_status st = step_args(ctx, batch, hidden, XGR_DTYPE_BF16, rows, ldh, "step_head", a, rows_live, d);
+  if (st != XGR_OK) return st;
+  if (ctx->cfg.nranks > 1) return fail(XGR_ERR_UNSUPPORTED, "step_head: codebook-sharded ctx");
+  int64_t keys = 0;
+  if (a.t == 1 || !next_is_sparse(ctx, &keys))
+    return fail(XGR_ERR_UNSUPPORTED, "step_head: step %d is not a sparse step after the root (see xgr_beam_next_route)",
+                a.t);
+  cudaStream_t s = (cudaStream_t)stream;
+  a.clog = ctx->head_logits;
+  a.cld = ctx->trie.lv[a.t - 1].max_children;
+  a.sparse_cap = (int)keys;
+  int launches = 1;
+  ACK(xgr::launch_head(a, hidden, ldh, (int64_t)rows * ldh, head, ldw, bias, d, ctx->head_logits, s));
+  ACK(xgr::launch_sparse_compact(a, (int)keys, s, &launches));
+  ctx->launches += launches;
+  ctx->batch = batch;
+  ctx->step = a.t;
   ctx->last = a;
   ctx->last_rows = rows_live;
   return XGR_OK;

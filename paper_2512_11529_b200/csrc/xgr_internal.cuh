@@ -56,6 +56,10 @@ struct StepArgs {
   int32_t no_prune;
   int32_t sparse_cap;   // key capacity of k_sparse's dynamic shared memory
   int32_t dbg;          // XGR_DEBUG_FLAGS (experiments only; 0 in production)
+  // LM-head fusion (NEXT f4): the sparse step reads the legal logits from a compact buffer
+  // clog[batch][BW][cld] (child q of row b at (req*BW + b)*cld + q - first_child) instead of logits
+  const float* clog;
+  int32_t cld;
   // state in (null at t = 1: the root, one live beam with score 0)
   const float* score_in;
   const uint32_t* node_in;

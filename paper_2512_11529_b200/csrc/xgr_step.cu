@@ -1006,7 +1006,7 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
 // rows with <= 16 children (all rows' dependent load chains node -> first_child -> labels ->
 // logits run concurrently), and one warp per row for the rare larger rows.
 // ---------------------------------------------------------------------------------------------
-template <int T, bool ROOT, typename TI = float>
+template <int T, bool ROOT, typename TI = float, bool CMP = false>
 __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
   uint64_t* s_cand = s_dynk;
@@ -1122,12 +1122,13 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         continue;
       }
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const float* crow = CMP ? a.clog + ((size_t)req * a.BW + b) * a.cld : nullptr;
       uint32_t vv[kSmall];
       float xv[kSmall];
 #pragma unroll
       for (int k = 0; k < kSmall; ++k) vv[k] = k < cnt ? lab[fc + k] : 0u;
 #pragma unroll
-      for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? ldx(row + vv[k]) : -INFINITY;
+      for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? (CMP ? crow[k] : ldx(row + vv[k])) : -INFINITY;
       float M = -INFINITY;
 #pragma unroll
       for (int k = 0; k < kSmall; ++k) M = fmaxf(M, xv[k]);
@@ -1153,12 +1154,14 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       row_state(a, req, b, S, node);
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
       const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      const float* crow = CMP ? a.clog + ((size_t)req * a.BW + b) * a.cld - fc : nullptr;
+      auto xq = [&](uint32_t k) { return CMP ? crow[k] : ldx(row + lab[k]); };
       float tmax = -INFINITY;
-      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, ldx(row + lab[k]));
+      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, xq(k));
       const float M = warp_max(tmax);
       float z = 0.f;
       for (uint32_t k = fc + lane; k < fe; k += 32)
-        z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[k]), M), kLog2e));
+        z += ex2(__fmul_rn(__fsub_rn(xq(k), M), kLog2e));
       const float Z = warp_sum(z);
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
       const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
@@ -1168,7 +1171,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       base = __shfl_sync(0xffffffffu, base, 0);
       for (uint32_t k = fc + lane; k < fe; k += 32) {
         uint32_t v = lab[k];
-        s_keys[base + (k - fc)] = make_key(cand_score(S, ldx(row + v), lse), (uint32_t)b * V + v);
+        s_keys[base + (k - fc)] = make_key(cand_score(S, xq(k), lse), (uint32_t)b * V + v);
       }
     }
   }
@@ -1314,6 +1317,8 @@ cudaError_t configure_kernels(int cap) {
       (e = cudaFuncSetAttribute(k_sparse<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)) ||
       (e = cudaFuncSetAttribute(k_sparse<512, true, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)))
     return e;
+  if ((e = cudaFuncSetAttribute(k_sparse<512, false, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)))
+    return e;
   return cudaFuncSetAttribute(k_sparse<512, false, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               spk);
 }
@@ -1356,6 +1361,14 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   if (bf16) k_select<512, __nv_bfloat16><<<a.batch, 512, sel, s>>>(a);
   else k_select<512><<<a.batch, 512, sel, s>>>(a);
   *launches += 1;
+  return cudaGetLastError();
+}
+
+// LM-head fusion (NEXT f4): the sparse step over the compact legal logits a.clog written by k_head.
+cudaError_t launch_sparse_compact(const StepArgs& a, int sparse_keys, cudaStream_t s, int* launches) {
+  const size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
+  k_sparse<512, false, float, true><<<a.batch, 512, smem, s>>>(a);
+  ++*launches;
   return cudaGetLastError();
 }
 

@@ -27,8 +27,10 @@ from __future__ import annotations
 import heapq
 
 
-def heap_select(rows, bw: int, vocab: int):
+def heap_select(rows, bw: int, vocab: int, top_k: int | None = None):
     """rows: list over beams b of (S_b, [(c, v), ...]) with candidates in any order.
+    top_k: the per-beam Top-K lists the paper feeds the heap:
+    only each beam's first top_k candidates in descending order are visited.
 
     Returns (selected [(c, flat)], stats dict). Heap entries are keyed so the heap top is the
     minimum under the total order (c desc, flat asc): the smallest c, and among equal c the
@@ -42,6 +44,8 @@ def heap_select(rows, bw: int, vocab: int):
             beams_skipped = len(rows) - b
             break
         ordered = sorted(cands, key=lambda cv: (-cv[0], cv[1]))
+        if top_k is not None:
+            ordered = ordered[:top_k]
         for c, v in ordered:
             visits += 1
             flat = b * vocab + v

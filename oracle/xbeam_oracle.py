@@ -206,9 +206,28 @@ def step_candidates(vocab: Vocabulary, state: BeamState, logits):
             np.concatenate(vs), nonfinite)
 
 
-def beam_step(vocab: Vocabulary, state: BeamState, logits, bw: int) -> BeamState:
-    """One decode step of one request (DESIGN.md readings)."""
+def per_beam_topk(c, flat, b, k: int) -> np.ndarray:
+    """Indices of each beam's first min(k, n_b) candidates under (c desc, flat asc) -- within a
+    row that is (score desc, token asc) -- the per-beam Top-K of PAPER.md L156 (section 2.2.2,
+    "selects the Top-K most likely next-token candidates") and SPEC S:L356-364. Full sort."""
+    c = np.asarray(c, dtype=np.float64)
+    flat = np.asarray(flat, dtype=np.int64)
+    b = np.asarray(b, dtype=np.int64)
+    order = np.lexsort((flat, -c, b))            # by beam, then (c desc, flat asc)
+    bo = b[order]
+    start = np.searchsorted(bo, bo, side="left")  # first index of each element's beam run
+    rank = np.arange(order.shape[0]) - start
+    return np.sort(order[rank < k])
+
+
+def beam_step(vocab: Vocabulary, state: BeamState, logits, bw: int, top_k: int | None = None) -> BeamState:
+    """One decode step of one request (DESIGN.md readings).
+    top_k (NEXT f3): keep each beam's Top-K candidates first, then the global
+    Top-BW of that BW x K pool; None or top_k >= BW is the plain definition (reading R3)."""
     c, flat, b, v, nonfinite = step_candidates(vocab, state, logits)
+    if top_k is not None and top_k < bw:
+        keep = per_beam_topk(c, flat, b, top_k)
+        c, flat, b, v = c[keep], flat[keep], b[keep], v[keep]
     sel = select_top_bw(c, flat, bw)
     parents = b[sel]
     tokens = v[sel]
@@ -237,13 +256,13 @@ def finalize(vocab: Vocabulary, state: BeamState, bw: int) -> FinalItems:
     return FinalItems(tokens=tok, item_rank=rank, scores=sc, n_live=state.n_live)
 
 
-def run_request(vocab: Vocabulary, logits_per_step, bw: int):
+def run_request(vocab: Vocabulary, logits_per_step, bw: int, top_k: int | None = None):
     """Free-running ND-step beam search of one request. logits_per_step[t] is [rows][ld]
     (row 0 only at t = 0). Returns (FinalItems, [BeamState after each step])."""
     state = BeamState.root()
     states = []
     for t in range(vocab.nd):
-        state = beam_step(vocab, state, logits_per_step[t], bw)
+        state = beam_step(vocab, state, logits_per_step[t], bw, top_k)
         states.append(state)
     return finalize(vocab, state, bw), states
 

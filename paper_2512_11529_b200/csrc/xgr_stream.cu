@@ -118,7 +118,9 @@ struct Desc {
 
 // k_stream modes: normal step; codebook-shard stats pass (local (m, Z) per row, no emission);
 // codebook-shard emit pass (global lse given, no (m, Z) work).
-constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2;
+// kModeSeedHist: the histogram seed over rows b < R0 (only those rows are scheduled; no emission):
+// each row's candidates >= a row-local bound go to the request's histogram of S_0 - c.
+constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2, kModeSeedHist = 3;
 
 // Consumer-group reductions: warp butterfly, then every consumer thread folds the per-warp
 // partials in a fixed order (bitwise-identical, deterministic results in every thread).
@@ -688,6 +690,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
   __shared__ float s_th[NS];
   __shared__ float p_max[G][GT / 32], p_sum[G][GT / 32];
   __shared__ float2 part[G][2][GT / 32];
+  __shared__ float s_tau[G][GT / 32];
 
   const int tid = threadIdx.x;
   const int V = a.trie.V;
@@ -738,7 +741,8 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         m.live = m.b < nl;
         if (m.live) {
           row_state(a, m.req, m.b, m.S, m.node);
-          if (MODE != kModeStats) m.th = theta_value(a.theta[m.req]);
+          if (MODE != kModeStats && MODE != kModeSeedHist) m.th = theta_value(a.theta[m.req]);
+          if (MODE == kModeSeedHist) m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
           if (MODE == kModeShardEmit) {
             bool fin;
             m.lse = shard_lse(a, m.req, m.b, fin);
@@ -873,7 +877,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
     if (d.kind != 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      if (d.kind == 0) continue;
+      if (d.kind == 0 || MODE == kModeSeedHist) continue;   // sparse seed rows add no bound
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
@@ -995,6 +999,62 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
       continue;
     }
+    if (MODE == kModeSeedHist) {
+      // rows b < R0: candidates >= a row-local bound tau into the request's histogram of S_0 - c
+      // (bins of 1/128). tau: each warp's m-th largest (m = ceil(BW / 8) <= 64) of its lanes'
+      // top-2 candidates -- distinct elements, so the row has >= BW candidates >= tau.
+      if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
+      const float lse3 = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      const float S0 = d.lse;
+      float c1 = -INFINITY, c2 = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        x[e] = cand_score(S, x[e], lse3);
+        c2 = fmaxf(c2, fminf(c1, x[e]));
+        c1 = fmaxf(c1, x[e]);
+      }
+      const int mm = (BW + GT / 32 - 1) / (GT / 32);
+      float tau = -INFINITY;
+      if (mm <= 64) {
+        float A = c1, B = c2;
+#pragma unroll
+        for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+          for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            const float oa = __shfl_xor_sync(0xffffffffu, A, stride);
+            const float ob = __shfl_xor_sync(0xffffffffu, B, stride);
+            const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
+            A = keep_max ? fmaxf(A, oa) : fminf(A, oa);
+            B = keep_max ? fmaxf(B, ob) : fminf(B, ob);
+          }
+        }
+        float best = -INFINITY;
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int i = lane + 32 * hh, j = mm - i;
+          const float av = __shfl_sync(0xffffffffu, A, (i - 1) & 31);
+          const float bv = __shfl_sync(0xffffffffu, B, (j - 1) & 31);
+          if (i <= 32 && j >= 0 && j <= 32) best = fmaxf(best, fminf(i > 0 ? av : INFINITY, j > 0 ? bv : INFINITY));
+        }
+        best = wmax(best);
+        if (lane == 0) s_tau[g][lt >> 5] = best;
+        named_sync(bar_id, GT);
+        tau = s_tau[g][0];
+#pragma unroll
+        for (int w2 = 1; w2 < GT / 32; ++w2) tau = fminf(tau, s_tau[g][w2]);
+      }
+      if (c1 >= tau && c1 > -INFINITY) {
+        uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+#pragma unroll
+        for (int e = 0; e < EPT; ++e) {
+          if (x[e] >= tau && x[e] > -INFINITY) {
+            const float dd = __fmul_rn(__fsub_rn(S0, x[e]), 128.0f);
+            if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(h + (int)dd, 1u);
+          }
+        }
+      }
+      continue;
+    }
     const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
     lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
     if (lt == 0) {
@@ -1106,6 +1166,7 @@ static size_t stream_smem() {
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
+static int g_seed_kernel = 0;      // XGR_SEED_KERNEL: 0 seed rows streamed (k_stream seed mode), 1 k_seed_hist
 static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>
@@ -1135,6 +1196,11 @@ cudaError_t configure_stream_kernels() {
     return e;
   if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
   if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
+  if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
+  if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 4, 3, kModeSeedHist, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
+      cudaSuccess)
+    return e;
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
@@ -1168,7 +1234,11 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     using bf = __nv_bfloat16;
     const int r0 = std::min(a.theta_rows, rows);
     if (r0 > 0) {
-      if (a.trie.V <= 8192) k_seed_hist<256, 4, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      const int ns = a.batch * r0;
+      if (a.trie.V <= 8192 && g_seed_kernel != 1)
+        k_stream<32, 1, 4, 3, kModeSeedHist, bf><<<std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s>>>(
+            a, ns, 0);
+      else if (a.trie.V <= 8192) k_seed_hist<256, 4, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
       else k_seed_hist<256, 8, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
       ++*launches;
     }
@@ -1189,7 +1259,12 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     if (g_seed_mode == 1) {   // histogram seed over rows 0..R0-1; every row is then streamed
       const int r0 = std::min(a.theta_rows, rows);
       if (r0 > 0) {
-        k_seed_hist<256, 8><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+        if (g_seed_kernel == 1) {   // XGR_SEED_KERNEL=1: one CTA per seed row
+          k_seed_hist<256, 8><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+        } else {                    // the seed rows streamed by the persistent kernel
+          const int ns = a.batch * r0;
+          k_stream<32, 1, 2, 3, kModeSeedHist><<<std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, ns, 0);
+        }
         ++*launches;
       }
       k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);

@@ -51,7 +51,7 @@ typedef struct xgr_ctx xgr_ctx; /* opaque; one per in-flight batch */
 typedef enum {
   XGR_OK = 0,
   XGR_ERR_INVALID_ARG = 1, /* null pointer, size out of range, bad config */
-  XGR_ERR_UNSUPPORTED = 2, /* valid but not implemented (0 < top_k < BW, nranks > 1, ...) */
+  XGR_ERR_UNSUPPORTED = 2, /* valid but not implemented (0 < top_k < BW with nranks > 1, ...) */
   XGR_ERR_TOKEN_RANGE = 3, /* mask_build: a token < 0 or >= V */
   XGR_ERR_EMPTY_VOCAB = 4, /* mask_build: zero items (no beam could live) */
   XGR_ERR_SEQUENCE = 5,    /* call out of order */
@@ -72,7 +72,8 @@ typedef struct {
   int32_t vocab;      /* V: tokens per level, 1..65536                                   */
   int32_t nd;         /* ND: tokens per item (trie depth), 1..8; nd*ceil(log2 V) <= 64    */
   int32_t beam_width; /* BW, 1..1024                                                      */
-  int32_t top_k;      /* per-beam K. 0 or >= BW: no truncation (v1 only)  */
+  int32_t top_k;      /* per-beam K: each beam keeps its K best candidates
+                         (score desc, token asc) before the global Top-BW. 0 or >= BW: none */
   int32_t max_batch;  /* max requests per step call, >= 1                                 */
   int32_t device;     /* CUDA device ordinal                                             */
   int32_t nranks;     /* codebook shards G >= 1 (1: no shard). G > 1: V % G == 0 and       */

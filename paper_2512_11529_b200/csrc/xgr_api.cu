@@ -31,7 +31,7 @@ using namespace xgr;
 
 struct xgr_ctx {
   xgr_config cfg;
-  int V = 0, nd = 0, BW = 0, maxB = 0, cap = 0, R0 = 0;
+  int V = 0, nd = 0, BW = 0, maxB = 0, cap = 0, R0 = 0, K = 0;
   TrieHost trie;
   bool built = false;
   float* score[2] = {nullptr, nullptr};
@@ -145,8 +145,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.beam_width < 1 || c.beam_width > kMaxBW)
     return fail(XGR_ERR_INVALID_ARG, "init: beam_width %d not in 1..1024", c.beam_width);
   if (c.top_k < 0) return fail(XGR_ERR_INVALID_ARG, "init: top_k < 0");
-  if (c.top_k > 0 && c.top_k < c.beam_width)
-    return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width is not implemented (v1)");
+  if (c.top_k > 0 && c.top_k < c.beam_width && c.nranks > 1)
+    return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width with the codebook shard");
   if (c.max_batch < 1) return fail(XGR_ERR_INVALID_ARG, "init: max_batch < 1");
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks)
     return fail(XGR_ERR_INVALID_ARG, "init: need 0 <= rank < nranks");
@@ -181,6 +181,7 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
     return fail(XGR_ERR_INVALID_ARG, "init: survivor_cap > 16384");
   }
   x->R0 = c.theta_rows ? c.theta_rows : 8;
+  x->K = (c.top_k > 0 && c.top_k < c.beam_width) ? c.top_k : 0;   // 0: no per-beam truncation
   const size_t nb = (size_t)x->maxB * x->BW;
   auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
   cudaError_t e = cudaSuccess;
@@ -292,6 +293,7 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   a.batch = batch;
   a.cap = ctx->cap;
   a.theta_rows = ctx->R0;
+  a.topk = ctx->K;
   a.counters_on = (ctx->cfg.flags & XGR_CFG_COUNTERS) ? 1 : 0;
   a.no_prune = (ctx->cfg.flags & XGR_CFG_NO_PRUNE) ? 1 : 0;
   a.col0 = ctx->cfg.rank * Vl;

@@ -52,6 +52,7 @@ struct StepArgs {
   int32_t batch;
   int32_t cap;          // survivor buffer capacity per request (keys)
   int32_t theta_rows;
+  int32_t topk;         // per-beam Top-K (NEXT f3): 0 = none (K >= BW), else each row keeps its best K
   int32_t counters_on;
   int32_t no_prune;
   int32_t sparse_cap;   // key capacity of k_sparse's dynamic shared memory

@@ -492,14 +492,17 @@ __device__ int block_topk_fast(uint64_t* keys, int n, int k, uint64_t* cand, int
 }
 
 // Parent-row trie info for the commit, fetched at kernel start (overlaps the selection work).
-struct ParentInfo {
-  uint32_t fc[kMaxBW];
-  uint32_t fcn[kMaxBW];
-  int32_t slot[kMaxBW];
+// N = 1 for the root step (one parent), which keeps k_sparse<ROOT> at two CTAs per SM.
+template <int N>
+struct ParentInfoN {
+  uint32_t fc[N];
+  uint32_t fcn[N];
+  int32_t slot[N];
 };
+using ParentInfo = ParentInfoN<kMaxBW>;
 
-template <int T>
-__device__ void prefetch_parents(const StepArgs& a, int req, int nl, ParentInfo& pi) {
+template <int T, typename PI>
+__device__ void prefetch_parents(const StepArgs& a, int req, int nl, PI& pi) {
   const LevelDev& L = a.trie.lv[a.level];
   for (int b = threadIdx.x; b < nl; b += T) {
     const uint32_t node = a.node_in ? a.node_in[(size_t)req * a.BW + b] : 0u;
@@ -512,8 +515,8 @@ __device__ void prefetch_parents(const StepArgs& a, int req, int nl, ParentInfo&
 }
 
 // Commit the k selected keys (sorted desc) of request req into the step-t state (a5).
-template <int T>
-__device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, const ParentInfo& pi) {
+template <int T, typename PI>
+__device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, const PI& pi) {
   const int V = a.trie.V;
   const size_t base = (size_t)req * a.BW;
   if (a.rec_out) {   // codebook-shard select phase: this rank's local top-BW keys, no state update
@@ -841,14 +844,16 @@ __device__ __forceinline__ void for_each_candidate(const StepArgs& a, int req, i
   }
 }
 
+// Exact top-k (k <= kMaxBW) of the request's candidates with key >= the theta key and key < hi,
+// by streaming its rows once per 8-bit radix digit (at most 8 passes); sorted into s_out. Returns
+// how many there are (< k when fewer exist).
 template <int T, typename TI>
-__device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uint64_t* s_out,
-                                uint32_t* s_hist, uint32_t* s_m32, const ParentInfo& s_pi) {
+__device__ int fallback_topk(const StepArgs& a, int req, int k, uint64_t hi, uint64_t* s_sel, uint64_t* s_out,
+                             uint32_t* s_hist, uint32_t* s_m32) {
   const int tid = threadIdx.x;
   const int nl = nlive_of(a, req);
   const float th = theta_value(a.theta[req]);
   const uint64_t klo = (uint64_t)a.theta[req] << 32;
-  const int k = a.BW;  // overflow => more than cap >= BW candidates >= theta
   uint64_t prefix = 0, mask = 0;
   uint32_t krem = (uint32_t)k;
   for (int shift = 56; shift >= 0; shift -= 8) {
@@ -861,14 +866,14 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
       const float lse = a.lse[(size_t)req * a.BW + b];
       if (S < th || lse != lse) continue;
       for_each_candidate<T, TI>(a, req, b, S, lse, node, [&](uint64_t key) {
-        if (key >= klo && (key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 0xFFu], 1u);
+        if (key >= klo && key < hi && (key & mask) == prefix) atomicAdd(&s_hist[(key >> shift) & 0xFFu], 1u);
       });
     }
     __syncthreads();
     if (tid < 32) warp_find_digit_desc(s_hist, krem, &s_m32[0], &s_m32[1]);
     __syncthreads();
     uint32_t d = s_m32[0], above = s_m32[1];
-    if (d >= 256) {   // fewer candidates than BW (flagged request): take them all
+    if (d >= 256) {   // fewer candidates than k: take them all
       krem = 0;
       prefix = 0;
       mask = 0;
@@ -892,7 +897,7 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
     const float lse = a.lse[(size_t)req * a.BW + b];
     if (S < th || lse != lse) continue;
     for_each_candidate<T, TI>(a, req, b, S, lse, node, [&](uint64_t key) {
-      if (key >= thr && key >= klo) {
+      if (key >= thr && key >= klo && key < hi) {
         uint32_t p = atomicAdd(&s_m32[2], 1u);
         if (p < (uint32_t)k) s_sel[p] = key;
       }
@@ -901,12 +906,36 @@ __device__ void fallback_select(const StepArgs& a, int req, uint64_t* s_sel, uin
   __syncthreads();
   const int kk = min(k, (int)s_m32[2]);
   sort_desc_to<T>(s_sel, kk, s_out);
-  commit<T>(a, req, s_out, kk, s_pi);
+  return kk;
 }
 
-// ---------------------------------------------------------------------------------------------
-// k_select: per request, top-BW of the survivors (a4) and commit (a5).
-// ---------------------------------------------------------------------------------------------
+// Per-beam Top-K (NEXT f3) over keys sorted descending: one warp walks them in order with a
+// counter per parent row; a key is kept iff fewer than K keys of its row came before it. Kept
+// keys are appended to res (in order, so res stays sorted) until BW are kept. Warp 0 only; the
+// counters (cnt[BW]) and *nres persist across calls (chunks of one request).
+__device__ void topk_scan(const uint64_t* keys, int m, int K, int V, int BW, int* cnt, uint64_t* res, int* nres) {
+  const int lane = lane_id();
+  int n = *nres;
+  for (int base = 0; base < m && n < BW; base += 32) {
+    const int i = base + lane;
+    const bool valid = i < m;
+    const uint64_t key = valid ? keys[i] : 0ull;
+    const int b = valid ? (int)(key_flat(key) / (uint32_t)V) : -1 - lane;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    const uint32_t lt = (1u << lane) - 1u;
+    const int c0 = valid ? cnt[b] : 0;
+    const bool keep = valid && c0 + __popc(peers & lt) < K;
+    __syncwarp();
+    if (valid && lane == 31 - __clz(peers)) cnt[b] = c0 + __popc(peers);
+    const uint32_t kb = __ballot_sync(0xffffffffu, keep);
+    const int pos = n + __popc(kb & lt);
+    if (keep && pos < BW) res[pos] = key;
+    n += __popc(kb);
+    __syncwarp();
+  }
+  if (lane == 0) *nres = min(n, BW);
+}
+
 template <int T, typename TI = float>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
   extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
@@ -914,6 +943,9 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ TopkScratch s_sc;
   __shared__ ParentInfo s_pi;
+  __shared__ int s_nres;
+  int* s_rowcnt = reinterpret_cast<int*>(s_cand + kMaxBW);   // per-beam Top-K row counters [BW]
+                                                            // (results use s_cand[0 .. BW))
   const int req = blockIdx.x, tid = threadIdx.x;
   const uint64_t* src = a.surv + (size_t)req * a.cap;
   const uint64_t p0 = tid < a.cap ? src[tid] : 0ull;
@@ -933,7 +965,24 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
     }
     prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
     __syncthreads();
-    fallback_select<T, TI>(a, req, s_sel, s_out, s_sc.hist, s_sc.m32, s_pi);
+    if (!a.topk) {
+      const int kk = fallback_topk<T, TI>(a, req, a.BW, ~0ull, s_sel, s_out, s_sc.hist, s_sc.m32);
+      commit<T>(a, req, s_out, kk, s_pi);
+    } else {   // per-beam Top-K: chunks of the largest remaining candidates until BW are kept
+      for (int i = tid; i < a.BW; i += T) s_rowcnt[i] = 0;
+      if (tid == 0) s_nres = 0;
+      __syncthreads();
+      uint64_t hi = ~0ull;
+      for (;;) {
+        const int kk = fallback_topk<T, TI>(a, req, kMaxBW, hi, s_sel, s_out, s_sc.hist, s_sc.m32);
+        if (tid < 32) topk_scan(s_out, kk, a.topk, a.trie.V, a.BW, s_rowcnt, s_cand, &s_nres);
+        __syncthreads();
+        if (s_nres >= a.BW || kk < kMaxBW) break;
+        hi = s_out[kk - 1];
+        __syncthreads();
+      }
+      commit<T>(a, req, s_cand, s_nres, s_pi);
+    }
     return;
   }
   const int k = min((int)n, a.BW);
@@ -957,9 +1006,32 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   }
   __syncthreads();
   if (a.dbg & 128) return;
-  block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
-  if (a.dbg & 256) return;
-  commit<T>(a, req, s_out, k, s_pi);
+  if (!a.topk) {
+    block_topk_fast<T>(s_keys, (int)n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
+    if (a.dbg & 256) return;
+    commit<T>(a, req, s_out, k, s_pi);
+  } else {
+    // per-beam Top-K (NEXT f3): take the largest remaining survivors in sorted chunks of up to
+    // kMaxBW, keep those within their row's first K, until BW are kept; processed keys are zeroed
+    // (0 is below every real key), so each chunk is the next one in descending order
+    for (int i = tid; i < a.BW; i += T) s_rowcnt[i] = 0;
+    if (tid == 0) s_nres = 0;
+    __syncthreads();
+    int nz = (int)n;
+    while (nz > 0) {
+      const int kc = min(nz, kMaxBW);
+      block_select_topk<T>(s_keys, (int)n, kc, s_sel, s_out, s_sc.hist, s_sc.m64, s_sc.m32);
+      if (tid < 32) topk_scan(s_out, kc, a.topk, a.trie.V, a.BW, s_rowcnt, s_cand, &s_nres);
+      __syncthreads();
+      if (s_nres >= a.BW || kc == nz) break;
+      const uint64_t thr = s_out[kc - 1];
+      for (uint32_t i = tid; i < n; i += T)
+        if (s_keys[i] >= thr) s_keys[i] = 0ull;
+      nz -= kc;
+      __syncthreads();
+    }
+    commit<T>(a, req, s_cand, s_nres, s_pi);
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1013,10 +1085,12 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   uint64_t* s_keys = s_dynk + 2 * kMaxBW;
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ TopkScratch s_sc;
-  __shared__ ParentInfo s_pi;
+  constexpr int NR = ROOT ? 1 : kMaxBW;   // parent rows
+  __shared__ ParentInfoN<NR> s_pi;
   __shared__ float s_red[T / 32], s_red2[T / 32];
   __shared__ uint32_t s_count, s_nbig;
-  __shared__ int32_t s_big[kMaxBW];
+  __shared__ uint16_t s_rbase[NR], s_rcnt[NR];   // each row's key segment (per-beam Top-K)
+  __shared__ int32_t s_big[NR];
   const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
   // beam state of rows tid and tid + T loaded speculatively, alongside nlive
   static_assert(2 * T >= kMaxBW, "k_sparse: two rows per thread");
@@ -1141,6 +1215,8 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
       const uint32_t base = atomicAdd(&s_count, (uint32_t)cnt);
       XGR_CHECK(base + cnt <= (uint32_t)a.sparse_cap, "sparse keys base %u cnt %d cap %d", base, cnt, a.sparse_cap);
+      s_rbase[b] = (uint16_t)base;
+      s_rcnt[b] = (uint16_t)cnt;
 #pragma unroll
       for (int k = 0; k < kSmall; ++k)
         if (k < cnt) s_keys[base + k] = make_key(cand_score(S, xv[k], lse), (uint32_t)b * V + vv[k]);
@@ -1167,7 +1243,11 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
       if (!finite && lane == 0) atomicOr(a.flags + req, kFlagNonfinite);
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&s_count, fe - fc);
+      if (lane == 0) {
+        base = atomicAdd(&s_count, fe - fc);
+        s_rbase[b] = (uint16_t)base;
+        s_rcnt[b] = (uint16_t)(fe - fc);
+      }
       base = __shfl_sync(0xffffffffu, base, 0);
       for (uint32_t k = fc + lane; k < fe; k += 32) {
         uint32_t v = lab[k];
@@ -1178,7 +1258,39 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   __syncthreads();
   const int n = (int)s_count;
   if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
-  const int k = min(n, a.BW);
+  int k = min(n, a.BW);
+  if (a.topk) {
+    if (ROOT) {
+      k = min(k, a.topk);   // one row: its Top-K, then the Top-BW of those
+    } else {
+      // per-beam Top-K (NEXT f3): a key whose row segment holds >= K larger keys is dropped
+      // (zeroed: 0 is below every real key, so the selection below never takes it)
+      uint32_t* s_kill = s_sc.hist;   // scratch: 256 words, a bit per key in chunks of 8192
+      int killed = 0;
+      for (int c0 = 0; c0 < n; c0 += 8192) {
+        for (int i = tid; i < 256; i += T) s_kill[i] = 0u;
+        __syncthreads();
+        for (int i = c0 + tid; i < min(n, c0 + 8192); i += T) {
+          const uint64_t key = s_keys[i];
+          const int b = (int)(key_flat(key) / (uint32_t)V);
+          const int cnt = s_rcnt[b];
+          if (cnt > a.topk) {
+            const int base = s_rbase[b];
+            int r = 0;
+            for (int j = base; j < base + cnt; ++j) r += s_keys[j] > key;
+            if (r >= a.topk) atomicOr(&s_kill[(i - c0) >> 5], 1u << ((i - c0) & 31));
+          }
+        }
+        __syncthreads();
+        for (int i = c0 + tid; i < min(n, c0 + 8192); i += T)
+          if ((s_kill[(i - c0) >> 5] >> ((i - c0) & 31)) & 1u) s_keys[i] = 0ull;
+        for (int w = tid; w < 256; w += T) killed += __popc(s_kill[w]);
+        __syncthreads();
+      }
+      killed = block_sum_i<T>(killed, reinterpret_cast<int*>(s_red));
+      k = min(n - killed, a.BW);
+    }
+  }
   block_topk_fast<T>(s_keys, n, k, s_cand, 2 * kMaxBW, s_sel, s_out, s_sc, a.dbg >> 10);
   commit<T>(a, req, s_out, k, s_pi);
 }
@@ -1289,7 +1401,7 @@ __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
 template <int T, int VPT>
 static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0,
                                 cudaEvent_t ev1, int* launches) {
-  if (!a.no_prune) {
+  if (!a.no_prune && !a.topk) {   // a single row's bound is no bound for the per-beam Top-K pool
     int r0 = min(a.theta_rows, rows);
     if (r0 > 0) {
       k_theta<T, VPT><<<dim3(a.batch, r0), T, 0, s>>>(a);

@@ -600,6 +600,36 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   }
   __syncthreads();
   uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+  if (a.topk) {
+    // per-beam Top-K (NEXT f3): the row contributes only its best K candidates -- the bins in
+    // order of d until the count reaches K, the last one partially (counts are all theta needs)
+    constexpr int PER = kSeedBins / T;
+    uint32_t c[PER], loc = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      c[j] = s_hist[tid * PER + j];
+      loc += c[j];
+    }
+    uint32_t incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    __syncthreads();   // s_tau is reused for the warp totals
+    if (lane == 31) reinterpret_cast<uint32_t*>(s_tau)[warp] = incl;
+    __syncthreads();
+    uint32_t before = incl - loc;
+    for (int w = 0; w < warp; ++w) before += reinterpret_cast<uint32_t*>(s_tau)[w];
+    const uint32_t K = (uint32_t)a.topk;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      const uint32_t take = before >= K ? 0u : min(c[j], K - before);
+      if (take) atomicAdd(h + tid * PER + j, take);
+      before += c[j];
+    }
+    return;
+  }
   for (int i = tid; i < kSeedBins; i += T) {
     const uint32_t v = s_hist[i];
     if (v) atomicAdd(h + i, v);
@@ -1235,7 +1265,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     const int r0 = std::min(a.theta_rows, rows);
     if (r0 > 0) {
       const int ns = a.batch * r0;
-      if (a.trie.V <= 8192 && g_seed_kernel != 1)
+      if (a.trie.V <= 8192 && g_seed_kernel != 1 && !a.topk)
         k_stream<32, 1, 4, 3, kModeSeedHist, bf><<<std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s>>>(
             a, ns, 0);
       else if (a.trie.V <= 8192) k_seed_hist<256, 4, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
@@ -1256,10 +1286,10 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   }
   if (a.trie.V <= 8192) {
     int seeded = g_seed_rows == 2 ? 2 : 4;
-    if (g_seed_mode == 1) {   // histogram seed over rows 0..R0-1; every row is then streamed
+    if (g_seed_mode == 1 || a.topk) {   // histogram seed over rows 0..R0-1; every row is then streamed
       const int r0 = std::min(a.theta_rows, rows);
       if (r0 > 0) {
-        if (g_seed_kernel == 1) {   // XGR_SEED_KERNEL=1: one CTA per seed row
+        if (g_seed_kernel == 1 || a.topk) {   // one CTA per seed row (XGR_SEED_KERNEL=1; Top-K cap)
           k_seed_hist<256, 8><<<dim3(a.batch, r0), 256, 0, s>>>(a);
         } else {                    // the seed rows streamed by the persistent kernel
           const int ns = a.batch * r0;
@@ -1285,6 +1315,15 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
         k_stream<32, 1, 2, 3><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, seeded);
     }
+  } else if (a.topk) {   // V > 8192 with per-beam Top-K: the capped histogram seed
+    const int r0 = std::min(a.theta_rows, rows);
+    if (r0 > 0) {
+      k_seed_hist<256, 16><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      ++*launches;
+    }
+    k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+    if (ev0) cudaEventRecord(ev0, s);
+    k_stream<64, 2, 3><<<grid, 2 * 256 + 32, stream_smem<64, 3>(), s>>>(a, total, 0);
   } else {
     k_seed<512, 2><<<a.batch, 1024, stream_smem<64, 2>(), s>>>(a);
     if (ev0) cudaEventRecord(ev0, s);

@@ -9,6 +9,9 @@ adjudicated near-tie does not cascade. Comparison of one request's step:
      threshold are adjudicated by the oracle's fp64 recompute"): every pair in G \\ O and O \\ G
      has |c64 - theta64| <= tol(theta64); selected fp64 scores are non-increasing within tol;
      GPU scores within tol of their fp64 recompute.
+With a per-beam Top-K (NEXT f3) the oracle truncates each row to its K best first; a pair may
+then also differ when it lies within tol of its row's K-th fp64 score (the row cut, the same
+near-tie adjudication applied at the per-row boundary).
 """
 from __future__ import annotations
 
@@ -25,16 +28,25 @@ class ParityFailure(AssertionError):
     pass
 
 
-def compare_step(voc, state, logits_r, bw, g_par, g_tok, g_score, g_nlive, where=""):
+def compare_step(voc, state, logits_r, bw, g_par, g_tok, g_score, g_nlive, where="", top_k=None):
     """Returns 'strict' or 'adjudicated'; raises ParityFailure otherwise."""
     c, flat, b, v, nonfinite = O.step_candidates(voc, state, logits_r)
+    c_all, b_all, v_all = c, b, v
+    rowcut = {}
+    if top_k is not None and top_k < bw:
+        keep = O.per_beam_topk(c, flat, b, top_k)
+        for bb in np.unique(b):
+            m = b[keep] == bb
+            if np.count_nonzero(b == bb) > top_k:
+                rowcut[int(bb)] = float(np.min(c[keep][m]))
+        c, flat, b, v = c[keep], flat[keep], b[keep], v[keep]
     sel = O.select_top_bw(c, flat, bw)
     n_o = len(sel)
     if int(g_nlive) != n_o:
         raise ParityFailure(f"{where}: n_live gpu {g_nlive} != oracle {n_o}")
     o_pairs = list(zip(b[sel].tolist(), v[sel].tolist()))
     g_pairs = list(zip(np.asarray(g_par[:n_o]).tolist(), np.asarray(g_tok[:n_o]).tolist()))
-    c64 = {(int(bb), int(vv)): float(cc) for bb, vv, cc in zip(b, v, c)}
+    c64 = {(int(bb), int(vv)): float(cc) for bb, vv, cc in zip(b_all, v_all, c_all)}
     gs = np.asarray(g_score[:n_o], dtype=np.float64)
     # dead slots
     if np.any(np.asarray(g_par[n_o:]) != -1) or np.any(np.asarray(g_tok[n_o:]) != -1):
@@ -50,7 +62,8 @@ def compare_step(voc, state, logits_r, bw, g_par, g_tok, g_score, g_nlive, where
         return "strict"
     theta64 = c64[o_pairs[-1]]
     for p in set(g_pairs) ^ set(o_pairs):
-        if abs(c64[p] - theta64) > tol(theta64):
+        cut = rowcut.get(p[0])
+        if abs(c64[p] - theta64) > tol(theta64) and (cut is None or abs(c64[p] - cut) > tol(cut)):
             raise ParityFailure(f"{where}: set differs at {p} (c64 {c64[p]!r}, theta64 {theta64!r})")
     for j in range(n_o - 1):
         a, bnext = c64[g_pairs[j]], c64[g_pairs[j + 1]]

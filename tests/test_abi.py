@@ -56,7 +56,7 @@ def _cfg(**kw):
 @pytest.mark.parametrize("kw,status", [
     (dict(vocab=0), 1), (dict(vocab=65537), 1), (dict(nd=0), 1), (dict(nd=9), 1),
     (dict(beam_width=0), 1), (dict(beam_width=1025), 1), (dict(max_batch=0), 1),
-    (dict(top_k=2), 2), (dict(nranks=2), 2), (dict(vocab=65536, nd=5), 2), (dict(flags=0x80), 1), (dict(reserved=(ctypes.c_int32 * 5)(1, 0, 0, 0, 0)), 1),
+    (dict(top_k=-1), 1), (dict(top_k=2, nranks=2, vocab=1024, beam_width=8), 2), (dict(nranks=2), 2), (dict(vocab=65536, nd=5), 2), (dict(flags=0x80), 1), (dict(reserved=(ctypes.c_int32 * 5)(1, 0, 0, 0, 0)), 1),
 ])
 def test_init_validation_without_gpu(kw, status):
     from paper_2512_11529_b200 import binding

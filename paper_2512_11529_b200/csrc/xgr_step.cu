@@ -1126,10 +1126,11 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         // all loads issued up front: labels, then the logits they select
         uint32_t vv[RPT];
         float xv[RPT];
+        const bool all_legal = fe - fc == (uint32_t)V;   // labels are then 0..V-1: no label loads
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
           const uint32_t q = fc + (uint32_t)(k * T + tid);
-          vv[k] = q < fe ? (uint32_t)lab[q] : 0u;
+          vv[k] = q < fe ? (all_legal ? q - fc : (uint32_t)lab[q]) : 0u;
         }
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {

@@ -15,4 +15,8 @@ from .inputs import (  # noqa: F401
     make_logits,
     make_logits_torch,
     prefix_keyed_row,
+    ATTN_CONFIGS,
+    to_bf16_grid,
+    bf16_bits,
+    make_attn_inputs,
 )

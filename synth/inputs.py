@@ -140,3 +140,40 @@ def prefix_keyed_row(seed: int, request: int, prefix, vocab: int) -> np.ndarray:
     for k in range(4):
         s += ((r >> np.uint64(16 * k)) & np.uint64(0xFFFF)).astype(np.int64)
     return ((s - 131070).astype(np.float32) * np.float32(2.0 ** -15)).astype(np.float32)
+
+
+# ---- staged attention (second workload) ----------------------------------
+# Attention-layer shapes of the paper's largest evaluated model family (Qwen3 up to
+# 4B; Qwen3-4B: 32 query heads, 8 KV heads, head_dim 128) at the paper's memory-study point
+# (input length 1k, BW 256; ND = 3 decode phases).
+ATTN_CONFIGS = {
+    "A1": dict(n_req=2, bw=4, hq=4, hkv=2, d=128, ls=70, nd=3),          # tiny parity case
+    "A2": dict(n_req=16, bw=256, hq=32, hkv=8, d=128, ls=1024, nd=3),    # bench workload
+}
+
+
+def to_bf16_grid(x: np.ndarray) -> np.ndarray:
+    """Round fp32 values to the nearest bf16 (ties to even) and return them as fp32, so both sides
+    see the identical bf16 numbers (the CUDA side receives x.view(uint32) >> 16)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    r = (u + np.uint64(0x7FFF) + ((u >> np.uint64(16)) & np.uint64(1))) & np.uint64(0xFFFF0000)
+    return r.astype(np.uint32).view(np.float32)
+
+
+def bf16_bits(x: np.ndarray) -> np.ndarray:
+    """uint16 bf16 bit patterns of values already on the bf16 grid (to_bf16_grid)."""
+    return (np.ascontiguousarray(x, dtype=np.float32).view(np.uint32) >> np.uint32(16)).astype(np.uint16)
+
+
+def make_attn_inputs(n_req: int, bw: int, hq: int, hkv: int, d: int, ls: int, nd: int, seed: int,
+                     sigma_q: float = 1.0):
+    """Seeded bf16-grid inputs of one decode step's attention layer (values as fp32 arrays):
+    q [n_req][bw][hq][d] ~ sigma_q N(0,1); shared k, v [n_req][ls][hkv][d] ~ N(0,1) (the prompt's
+    KV after prefill, token-major); unshared k, v [n_req][bw][nd][hkv][d] ~ N(0,1) (each beam's
+    generated tokens: capacity BW x ND)."""
+    rng = np.random.default_rng(seed)
+    g = lambda *s: to_bf16_grid(rng.standard_normal(size=s, dtype=np.float32))
+    q = to_bf16_grid(rng.standard_normal(size=(n_req, bw, hq, d), dtype=np.float32) * np.float32(sigma_q))
+    ks, vs = g(n_req, ls, hkv, d), g(n_req, ls, hkv, d)
+    ku, vu = g(n_req, bw, nd, hkv, d), g(n_req, bw, nd, hkv, d)
+    return q, ks, vs, ku, vu

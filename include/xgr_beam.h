@@ -261,6 +261,56 @@ xgr_status xgr_kv_reorder(void* cache, int32_t n_req, int32_t n_panel, int32_t b
                           int64_t beam_stride, int64_t panel_stride, int64_t req_stride,
                           const int32_t* src, int32_t src_ld, void* stream);
 
+/* ---- Staged shared/unshared decode attention (second workload; PAPER.md
+ * L339, section 5.2 "Staged Computation Allocation"; L324 KV cache separation; SPEC.md
+ * S:L136-179). One decode step of one attention layer for n_req requests of bw beams:
+ *   out[r][b][h] = softmax_j(scale * q[r][b][h] . k_j) v_j over j in the request's prompt
+ *   positions (shared cache, one copy per request) followed by beam b's own generated tokens
+ *   t < n_unshared (unshared cache), with query head h reading KV head h / (hq / hkv).
+ * Layouts (DEVICE memory, bf16, element offsets; head_dim d = 128 only):
+ *   q        [n_req][bw][hq][d] contiguous
+ *   k_shared, v_shared  [n_req][ls][hkv][d] contiguous (prefill output, token-major)
+ *   k_unshared, v_unshared: element (r, b, t, g, e) at base + r*u_req_stride + b*u_beam_stride
+ *            + (t*hkv + g)*d + e (the unshared cache of PAPER.md L324, e.g. one layer's K or V
+ *            panel of the cache xgr_kv_reorder moves; strides multiples of 8 elements)
+ *   out      bf16 [n_req][bw][hq][d];  lse: fp32 [n_req][bw][hq] natural-log LSE, or NULL
+ * The shared stage runs on the tensor cores (tcgen05, fp32 accumulation; softmax weights are
+ * rounded to bf16 for the P.V product); the unshared stage and the merge run in its epilogue.
+ * Constraints: d == 128, hq % hkv == 0, G = hq / hkv a power of two <= 128, 1 <= bw <= 65535,
+ * n_req <= 65535, hkv <= 65535, 0 <= n_unshared <= 8, ls >= 0, ls + n_unshared >= 1 (S:L170:
+ * both stages empty is undefined), all pointers 16-byte aligned. Enqueues only (no sync, no
+ * allocation; graph-capturable). Errors: XGR_ERR_INVALID_ARG, XGR_ERR_UNSUPPORTED (d != 128 or
+ * G not a power of two), XGR_ERR_ALIGNMENT, XGR_ERR_CUDA. */
+xgr_status xgr_attn_staged(const void* q, const void* k_shared, const void* v_shared, int32_t ls,
+                           const void* k_unshared, const void* v_unshared, int64_t u_req_stride,
+                           int64_t u_beam_stride, int32_t n_unshared, void* out, float* lse,
+                           int32_t n_req, int32_t bw, int32_t hq, int32_t hkv, int32_t d, float scale,
+                           void* stream);
+
+/* Shared stage alone (SPEC attend_shared): partials of every (r, b, h) over the
+ * prompt, fp32 DEVICE outputs m [n_req][bw][hq] (max of the scaled logits), s (sum of
+ * exp(logit - m)), o [n_req][bw][hq][d] (sum of exp(logit - m) v, unnormalised); ls == 0 gives
+ * the empty partial (m = -inf, s = 0, o = 0). Same kernel, layouts and constraints as
+ * xgr_attn_staged. */
+xgr_status xgr_attn_shared(const void* q, const void* k_shared, const void* v_shared, int32_t ls,
+                           float* m, float* s, float* o, int32_t n_req, int32_t bw, int32_t hq,
+                           int32_t hkv, int32_t d, float scale, void* stream);
+
+/* Unshared stage alone (SPEC attend_unshared): partials over beam b's own tokens
+ * t < n_unshared (0 gives the empty partial), same output layout as xgr_attn_shared. */
+xgr_status xgr_attn_unshared(const void* q, const void* k_unshared, const void* v_unshared,
+                             int64_t u_req_stride, int64_t u_beam_stride, int32_t n_unshared,
+                             float* m, float* s, float* o, int32_t n_req, int32_t bw, int32_t hq,
+                             int32_t hkv, int32_t d, float scale, void* stream);
+
+/* OnlineSoftmax merge of two partials (SPEC merge_partials): for rows i < rows,
+ * M = max(m1, m2), w_k = exp(m_k - M) (0 for an empty partial), out[i] = (o1 w1 + o2 w2) /
+ * (s1 w1 + s2 w2) (fp32 [rows][d]), lse[i] = M + ln(s1 w1 + s2 w2) if lse != NULL. A row with
+ * both partials empty yields NaN (undefined). d == 128. */
+xgr_status xgr_attn_merge(const float* m1, const float* s1, const float* o1, const float* m2,
+                          const float* s2, const float* o2, int64_t rows, int32_t d, float* out,
+                          float* lse, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,6 +15,10 @@ from .binding import (  # noqa: F401
     XGR_DTYPE_BF16,
     XGR_DTYPE_F32,
     kv_reorder,
+    attn_staged,
+    attn_shared,
+    attn_unshared,
+    attn_merge,
     lib,
     LIB_PATH,
 )

@@ -32,7 +32,8 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_step_ex
            "xgr_beam_history", "xgr_beam_request_status", "xgr_mask_children", "xgr_mask_info",
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
            "xgr_beam_kernel_times", "xgr_beam_outputs", "xgr_shard_stats", "xgr_shard_select",
-           "xgr_shard_merge", "xgr_kv_reorder", "xgr_beam_step_head", "xgr_beam_next_route"]
+           "xgr_shard_merge", "xgr_kv_reorder", "xgr_beam_step_head", "xgr_beam_next_route",
+           "xgr_attn_staged", "xgr_attn_shared", "xgr_attn_unshared", "xgr_attn_merge"]
 
 
 class XgrConfig(ctypes.Structure):
@@ -80,6 +81,12 @@ def _load():
         "xgr_kv_reorder": [VP, I32, I32, I32, I64, I64, I64, I64, VP, I32, VP],
         "xgr_beam_step_head": [VP, I32, VP, I32, I64, VP, I64, VP, I32, VP],
         "xgr_beam_next_route": [VP, VP],
+        "xgr_attn_staged": [VP, VP, VP, I32, VP, VP, I64, I64, I32, VP, VP, I32, I32, I32, I32, I32,
+                            ctypes.c_float, VP],
+        "xgr_attn_shared": [VP, VP, VP, I32, VP, VP, VP, I32, I32, I32, I32, I32, ctypes.c_float, VP],
+        "xgr_attn_unshared": [VP, VP, VP, I64, I64, I32, VP, VP, VP, I32, I32, I32, I32, I32,
+                              ctypes.c_float, VP],
+        "xgr_attn_merge": [VP, VP, VP, VP, VP, VP, I64, I32, VP, VP, VP],
     }
     for name, args in sig.items():
         f = getattr(lib, name)
@@ -418,6 +425,91 @@ def kv_reorder(cache, src, stream=None):
     _check(lib.xgr_kv_reorder(ctypes.c_void_p(cache.data_ptr()), n_req, n_panel, bw, e * es,
                               cache.stride(2) * es, cache.stride(1) * es, cache.stride(0) * es,
                               ctypes.c_void_p(src.data_ptr()), src.stride(0), ctypes.c_void_p(st.cuda_stream)))
+
+
+# ---- staged shared/unshared attention (xgr_attn_*) ----------
+def _ptr(t):
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+def _attn_shapes(q, ks):
+    import torch
+    if q.dtype != torch.bfloat16 or q.dim() != 4 or not q.is_contiguous():
+        raise ValueError("q must be contiguous bf16 [n_req][bw][hq][d]")
+    n_req, bw, hq, d = q.shape
+    if ks is not None and (ks.dtype != torch.bfloat16 or ks.dim() != 4 or not ks.is_contiguous()
+                           or ks.shape[0] != n_req or ks.shape[3] != d):
+        raise ValueError("shared k/v must be contiguous bf16 [n_req][ls][hkv][d]")
+    return n_req, bw, hq, d
+
+
+def _unshared_strides(ku):
+    """ku: bf16 view [n_req][bw][>= n][hkv][d] with contiguous (t, hkv, d) per beam."""
+    if ku is None:
+        return 0, 0
+    if ku.dim() != 5 or ku.stride(4) != 1 or ku.stride(3) != ku.shape[4] or ku.stride(2) != ku.shape[3] * ku.shape[4]:
+        raise ValueError("unshared k/v must be [n_req][bw][nd][hkv][d] with contiguous (nd, hkv, d)")
+    return ku.stride(0), ku.stride(1)
+
+
+def attn_staged(q, ks, vs, ku, vu, n_unshared, hkv, scale, out=None, lse=None, stream=None):
+    """One decode step of staged attention (xgr_attn_staged): shared stage on the tensor cores,
+    unshared stage + OnlineSoftmax merge in its epilogue. Returns the bf16 output
+    [n_req][bw][hq][d] (and fills lse [n_req][bw][hq] fp32 if given)."""
+    import torch
+    n_req, bw, hq, d = _attn_shapes(q, ks)
+    ls = 0 if ks is None else ks.shape[1]
+    rs, bs = _unshared_strides(ku)
+    if out is None:
+        out = torch.empty_like(q)
+    st = torch.cuda.current_stream() if stream is None else stream
+    _check(lib.xgr_attn_staged(_ptr(q), _ptr(ks), _ptr(vs), ls, _ptr(ku), _ptr(vu), rs, bs, n_unshared,
+                               _ptr(out), _ptr(lse), n_req, bw, hq, hkv, d, float(scale),
+                               ctypes.c_void_p(st.cuda_stream)))
+    return out
+
+
+def attn_shared(q, ks, vs, hkv, scale, stream=None):
+    """Shared stage partials (xgr_attn_shared): (m, s, o) fp32."""
+    import torch
+    n_req, bw, hq, d = _attn_shapes(q, ks)
+    ls = 0 if ks is None else ks.shape[1]
+    m = torch.empty((n_req, bw, hq), dtype=torch.float32, device=q.device)
+    s = torch.empty_like(m)
+    o = torch.empty((n_req, bw, hq, d), dtype=torch.float32, device=q.device)
+    st = torch.cuda.current_stream() if stream is None else stream
+    _check(lib.xgr_attn_shared(_ptr(q), _ptr(ks), _ptr(vs), ls, _ptr(m), _ptr(s), _ptr(o), n_req, bw, hq, hkv, d,
+                               float(scale), ctypes.c_void_p(st.cuda_stream)))
+    return m, s, o
+
+
+def attn_unshared(q, ku, vu, n_unshared, hkv, scale, stream=None):
+    """Unshared stage partials (xgr_attn_unshared): (m, s, o) fp32."""
+    import torch
+    n_req, bw, hq, d = _attn_shapes(q, None)
+    rs, bs = _unshared_strides(ku)
+    m = torch.empty((n_req, bw, hq), dtype=torch.float32, device=q.device)
+    s = torch.empty_like(m)
+    o = torch.empty((n_req, bw, hq, d), dtype=torch.float32, device=q.device)
+    st = torch.cuda.current_stream() if stream is None else stream
+    _check(lib.xgr_attn_unshared(_ptr(q), _ptr(ku), _ptr(vu), rs, bs, n_unshared, _ptr(m), _ptr(s), _ptr(o), n_req,
+                                 bw, hq, hkv, d, float(scale), ctypes.c_void_p(st.cuda_stream)))
+    return m, s, o
+
+
+def attn_merge(p1, p2, with_lse=False, stream=None):
+    """OnlineSoftmax merge of two partials (xgr_attn_merge): returns out fp32 [..., d] (and lse)."""
+    import torch
+    m1, s1, o1 = p1
+    m2, s2, o2 = p2
+    d = o1.shape[-1]
+    rows = m1.numel()
+    out = torch.empty_like(o1)
+    lse = torch.empty_like(m1) if with_lse else None
+    st = torch.cuda.current_stream() if stream is None else stream
+    _check(lib.xgr_attn_merge(_ptr(m1), _ptr(s1), _ptr(o1), _ptr(m2), _ptr(s2), _ptr(o2), rows, d, _ptr(out),
+                              _ptr(lse), ctypes.c_void_p(st.cuda_stream)))
+    return (out, lse) if with_lse else out
 
 
 class ShardedBeamSearch:

@@ -12,7 +12,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libxgr_beam.so")
-SOURCES = ["xgr_api.cu", "xgr_build.cu", "xgr_step.cu", "xgr_stream.cu", "xgr_kv.cu", "xgr_head.cu"]
+SOURCES = ["xgr_api.cu", "xgr_build.cu", "xgr_step.cu", "xgr_stream.cu", "xgr_kv.cu", "xgr_head.cu", "xgr_attn.cu"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

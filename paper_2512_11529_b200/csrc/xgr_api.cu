@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -692,5 +693,116 @@ extern "C" xgr_status xgr_kv_reorder(void* cache, int32_t n_req, int32_t n_panel
   if (beam_stride < row_bytes) return fail(XGR_ERR_INVALID_ARG, "kv_reorder: beam_stride < row_bytes");
   ACK(xgr::launch_kv_reorder(cache, n_req, n_panel, bw, row_bytes, beam_stride, panel_stride, req_stride, src,
                              src_ld, (cudaStream_t)stream));
+  return XGR_OK;
+}
+
+// ---- staged shared/unshared attention (NEXT f4, second workload) ----------------------------------
+namespace xgr {
+int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, const void* ku, const void* vu,
+                       int64_t u_req_stride, int64_t u_beam_stride, int n_unshared, void* out, float* lse,
+                       float* pm, float* ps, float* po, int n_req, int bw, int hq, int hkv, float scale,
+                       cudaStream_t stream);
+cudaError_t launch_attn_unshared(const void* q, const void* ku, const void* vu, int64_t u_req_stride,
+                                 int64_t u_beam_stride, int n, int n_req, int bw, int hq, int hkv, float scale,
+                                 float* pm, float* ps, float* po, cudaStream_t stream);
+cudaError_t launch_attn_merge(const float* m1, const float* s1, const float* o1, const float* m2, const float* s2,
+                              const float* o2, int64_t rows, float* out, float* lse, cudaStream_t stream);
+}
+
+static bool misaligned(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) != 0; }
+
+static xgr_status attn_check(const char* fn, const void* q, int32_t n_req, int32_t bw, int32_t hq, int32_t hkv,
+                             int32_t d, float scale) {
+  if (n_req < 0 || bw < 1 || bw > 65535 || n_req > 65535 || hq < 1 || hkv < 1 || hkv > 65535 || hq % hkv != 0 ||
+      !(scale > 0.f) || !std::isfinite(scale))
+    return fail(XGR_ERR_INVALID_ARG, "%s: n_req %d bw %d hq %d hkv %d scale %g", fn, n_req, bw, hq, hkv, (double)scale);
+  const int G = hq / hkv;
+  if (d != 128 || G > 128 || (G & (G - 1)) != 0)
+    return fail(XGR_ERR_UNSUPPORTED, "%s: needs d == 128 and hq / hkv a power of two <= 128 (d %d, G %d)", fn, d, G);
+  if (!q) return fail(XGR_ERR_INVALID_ARG, "%s: NULL q", fn);
+  if (misaligned(q)) return fail(XGR_ERR_ALIGNMENT, "%s: q not 16-byte aligned", fn);
+  return XGR_OK;
+}
+
+static xgr_status attn_check_unshared(const char* fn, const void* ku, const void* vu, int64_t rs, int64_t bs,
+                                      int32_t n) {
+  if (n < 0 || n > 8) return fail(XGR_ERR_INVALID_ARG, "%s: n_unshared %d not in [0, 8]", fn, n);
+  if (n == 0) return XGR_OK;
+  if (!ku || !vu || rs < 0 || bs < 0) return fail(XGR_ERR_INVALID_ARG, "%s: NULL unshared cache or negative stride", fn);
+  if (misaligned(ku) || misaligned(vu) || (rs & 7) || (bs & 7))
+    return fail(XGR_ERR_ALIGNMENT, "%s: unshared cache not 16-byte aligned or strides not multiples of 8", fn);
+  return XGR_OK;
+}
+
+extern "C" xgr_status xgr_attn_staged(const void* q, const void* k_shared, const void* v_shared, int32_t ls,
+                                      const void* k_unshared, const void* v_unshared, int64_t u_req_stride,
+                                      int64_t u_beam_stride, int32_t n_unshared, void* out, float* lse,
+                                      int32_t n_req, int32_t bw, int32_t hq, int32_t hkv, int32_t d, float scale,
+                                      void* stream) {
+  xgr_status st = attn_check("attn_staged", q, n_req, bw, hq, hkv, d, scale);
+  if (st != XGR_OK) return st;
+  st = attn_check_unshared("attn_staged", k_unshared, v_unshared, u_req_stride, u_beam_stride, n_unshared);
+  if (st != XGR_OK) return st;
+  if (ls < 0 || ls + n_unshared < 1)
+    return fail(XGR_ERR_INVALID_ARG, "attn_staged: ls %d, n_unshared %d (both stages empty is undefined)", ls, n_unshared);
+  if (!out) return fail(XGR_ERR_INVALID_ARG, "attn_staged: NULL out");
+  if (ls > 0 && (!k_shared || !v_shared)) return fail(XGR_ERR_INVALID_ARG, "attn_staged: NULL shared cache");
+  if (misaligned(out) || misaligned(k_shared) || misaligned(v_shared) || misaligned(lse))
+    return fail(XGR_ERR_ALIGNMENT, "attn_staged: pointers must be 16-byte aligned");
+  if (n_req == 0) return XGR_OK;
+  const void* ks = ls > 0 ? k_shared : q;   // ls == 0: maps need a valid base; no tile is loaded
+  const void* vs = ls > 0 ? v_shared : q;
+  const int r = xgr::launch_attn_shared(q, ks, vs, ls, k_unshared, v_unshared, u_req_stride, u_beam_stride,
+                                        n_unshared, out, lse, nullptr, nullptr, nullptr, n_req, bw, hq, hkv, scale,
+                                        (cudaStream_t)stream);
+  if (r == 1) return fail(XGR_ERR_CUDA, "attn_staged: cuTensorMapEncodeTiled failed");
+  if (r != 0) return fail(XGR_ERR_CUDA, "attn_staged: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return XGR_OK;
+}
+
+extern "C" xgr_status xgr_attn_shared(const void* q, const void* k_shared, const void* v_shared, int32_t ls,
+                                      float* m, float* s, float* o, int32_t n_req, int32_t bw, int32_t hq,
+                                      int32_t hkv, int32_t d, float scale, void* stream) {
+  xgr_status st = attn_check("attn_shared", q, n_req, bw, hq, hkv, d, scale);
+  if (st != XGR_OK) return st;
+  if (ls < 0 || !m || !s || !o) return fail(XGR_ERR_INVALID_ARG, "attn_shared: ls %d or NULL output", ls);
+  if (ls > 0 && (!k_shared || !v_shared)) return fail(XGR_ERR_INVALID_ARG, "attn_shared: NULL shared cache");
+  if (misaligned(k_shared) || misaligned(v_shared) || misaligned(o))
+    return fail(XGR_ERR_ALIGNMENT, "attn_shared: pointers must be 16-byte aligned");
+  if (n_req == 0) return XGR_OK;
+  const void* ks = ls > 0 ? k_shared : q;
+  const void* vs = ls > 0 ? v_shared : q;
+  const int r = xgr::launch_attn_shared(q, ks, vs, ls, nullptr, nullptr, 0, 0, 0, nullptr, nullptr, m, s, o, n_req,
+                                        bw, hq, hkv, scale, (cudaStream_t)stream);
+  if (r == 1) return fail(XGR_ERR_CUDA, "attn_shared: cuTensorMapEncodeTiled failed");
+  if (r != 0) return fail(XGR_ERR_CUDA, "attn_shared: launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+  return XGR_OK;
+}
+
+extern "C" xgr_status xgr_attn_unshared(const void* q, const void* k_unshared, const void* v_unshared,
+                                        int64_t u_req_stride, int64_t u_beam_stride, int32_t n_unshared, float* m,
+                                        float* s, float* o, int32_t n_req, int32_t bw, int32_t hq, int32_t hkv,
+                                        int32_t d, float scale, void* stream) {
+  xgr_status st = attn_check("attn_unshared", q, n_req, bw, hq, hkv, d, scale);
+  if (st != XGR_OK) return st;
+  st = attn_check_unshared("attn_unshared", k_unshared, v_unshared, u_req_stride, u_beam_stride, n_unshared);
+  if (st != XGR_OK) return st;
+  if (!m || !s || !o) return fail(XGR_ERR_INVALID_ARG, "attn_unshared: NULL output");
+  if (misaligned(o)) return fail(XGR_ERR_ALIGNMENT, "attn_unshared: o must be 16-byte aligned");
+  if (n_req == 0) return XGR_OK;
+  ACK(xgr::launch_attn_unshared(q, k_unshared, v_unshared, u_req_stride, u_beam_stride, n_unshared, n_req, bw, hq,
+                                hkv, scale, m, s, o, (cudaStream_t)stream));
+  return XGR_OK;
+}
+
+extern "C" xgr_status xgr_attn_merge(const float* m1, const float* s1, const float* o1, const float* m2,
+                                     const float* s2, const float* o2, int64_t rows, int32_t d, float* out,
+                                     float* lse, void* stream) {
+  if (rows < 0 || d != 128) return fail(rows < 0 ? XGR_ERR_INVALID_ARG : XGR_ERR_UNSUPPORTED, "attn_merge: rows %lld d %d", (long long)rows, d);
+  if (rows == 0) return XGR_OK;
+  if (!m1 || !s1 || !o1 || !m2 || !s2 || !o2 || !out) return fail(XGR_ERR_INVALID_ARG, "attn_merge: NULL pointer");
+  if (misaligned(o1) || misaligned(o2) || misaligned(out))
+    return fail(XGR_ERR_ALIGNMENT, "attn_merge: o1, o2, out must be 16-byte aligned");
+  ACK(xgr::launch_attn_merge(m1, s1, o1, m2, s2, o2, rows, out, lse, (cudaStream_t)stream));
   return XGR_OK;
 }

@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int nu = a.n_unshared;
       const __nv_bfloat16* kub = a.ku + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
       const __nv_bfloat16* vub = a.vu + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
+      mbar_wait(bar_q, 0);   // the q rows are read from the Q tile (T == 0: nothing else waited)
       if (row_ok) {
 #pragma unroll
         for (int t = 0; t < kMaxU; ++t) {

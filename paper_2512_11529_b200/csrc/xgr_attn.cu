@@ -164,6 +164,7 @@ struct AttnArgs {
   float* pm;                         // partial mode: [n_req][bw][hq] m, s and [..][d] o (fp32)
   float* ps;
   float* po;
+  int vu_smem;                       // fused: stage the beams' unshared V rows in the K ring
 };
 
 // grid: (ceil(bw*G/128), hkv, n_req); 192 threads; kSmem dynamic shared memory.
@@ -177,20 +178,24 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int T = (a.ls + kBN - 1) / kBN;
   const uint32_t sb = su32(smem);
   if (sb & 1023u) __trap();   // the 128-byte swizzle atoms need 1024-byte alignment
-  const uint32_t bar_q = sb + kOffBar, bar_kv_full = bar_q + 8, bar_kv_empty = bar_q + 24,
-                 bar_s_full = bar_q + 40, bar_p_full = bar_q + 56, bar_o_done = bar_q + 64;
+  // barriers: Q; K ring full/empty [2]; V ring full/empty [2]; S full [2]; P full; O done
+  const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 24,
+                 bar_v_full = bar_q + 40, bar_v_empty = bar_q + 56, bar_s_full = bar_q + 72,
+                 bar_p_full = bar_q + 88, bar_o_done = bar_q + 96, bar_vu = bar_q + 104;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
-    mbar_init(bar_kv_full, 1);
-    mbar_init(bar_kv_full + 8, 1);
-    mbar_init(bar_kv_empty, 1);
-    mbar_init(bar_kv_empty + 8, 1);
-    mbar_init(bar_s_full, 1);
-    mbar_init(bar_s_full + 8, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_k_full + 8 * i, 1);
+      mbar_init(bar_k_empty + 8 * i, 1);
+      mbar_init(bar_v_full + 8 * i, 1);
+      mbar_init(bar_v_empty + 8 * i, 1);
+      mbar_init(bar_s_full + 8 * i, 1);
+    }
     mbar_init(bar_p_full, 128);
     mbar_init(bar_o_done, 1);
+    mbar_init(bar_vu, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm_q);
     prefetch_map(&tm_k);
@@ -207,22 +212,44 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    // ===== TMA producer =====
+    // ===== TMA producers: lane 0 streams Q then K, lane 1 streams V. A K stage is released by the
+    // commit after its S MMA, a V stage after its PV MMA, so K_{j+2} is in flight while tile j's
+    // softmax runs. =====
     if (lane == 0) {
       mbar_expect_tx(bar_q, 2 * kQPanel);
       const int b0 = mt * (kBM / a.G);
       tma_load_4d(sb + kOffQ, &tm_q, bar_q, 0, kvh * a.G, b0, req);
       tma_load_4d(sb + kOffQ + kQPanel, &tm_q, bar_q, 64, kvh * a.G, b0, req);
+    }
+    if (lane < 2) {
+      const CUtensorMap* tm = lane == 0 ? &tm_k : &tm_v;
+      const uint32_t full0 = lane == 0 ? bar_k_full : bar_v_full;
+      const uint32_t empty0 = lane == 0 ? bar_k_empty : bar_v_empty;
+      const uint32_t buf0 = sb + (lane == 0 ? kOffK : kOffV);
       for (int j = 0; j < T; ++j) {
         const int s = j & 1, u = j >> 1;
-        if (j >= 2) mbar_wait(bar_kv_empty + 8 * s, (u + 1) & 1);
-        const uint32_t full = bar_kv_full + 8 * s;
-        mbar_expect_tx(full, 4 * kKVPanel);
-        const uint32_t kd = sb + kOffK + s * 2 * kKVPanel, vd = sb + kOffV + s * 2 * kKVPanel;
-        tma_load_4d(kd, &tm_k, full, 0, kvh, j * kBN, req);
-        tma_load_4d(kd + kKVPanel, &tm_k, full, 64, kvh, j * kBN, req);
-        tma_load_4d(vd, &tm_v, full, 0, kvh, j * kBN, req);
-        tma_load_4d(vd + kKVPanel, &tm_v, full, 64, kvh, j * kBN, req);
+        if (j >= 2) mbar_wait(empty0 + 8 * s, (u + 1) & 1);
+        const uint32_t full = full0 + 8 * s, dst = buf0 + s * 2 * kKVPanel;
+        mbar_expect_tx(full, 2 * kKVPanel);
+        tma_load_4d(dst, tm, full, 0, kvh, j * kBN, req);
+        tma_load_4d(dst + kKVPanel, tm, full, 64, kvh, j * kBN, req);
+      }
+      if (!kPartial && lane == 0 && a.vu_smem) {
+        // the epilogue's unshared V rows, staged in the K ring once its last tiles are consumed
+        for (int j = max(0, T - 2); j < T; ++j) mbar_wait(bar_k_empty + 8 * (j & 1), (j >> 1) & 1);
+        const int nb = kBM / a.G, b0 = mt * nb, nbv = min(nb, a.bw - b0), nu = a.n_unshared;
+        const uint32_t rs = (uint32_t)nu * 256 + 16;
+        mbar_expect_tx(bar_vu, (uint32_t)(nbv * nu * 256));
+        for (int bl = 0; bl < nbv; ++bl)
+          for (int t = 0; t < nu; ++t) {
+            const __nv_bfloat16* src = a.vu + (int64_t)req * a.u_req_stride + (int64_t)(b0 + bl) * a.u_beam_stride +
+                                       ((int64_t)t * a.hkv + kvh) * kD;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
+                    sb + kOffK + bl * rs + t * 256),
+                "l"(src), "r"(bar_vu)
+                : "memory");
+          }
       }
     }
   } else if (warp == 1) {
@@ -233,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(bar_q, 0);
       auto issue_s = [&](int j) {
         const int s = j & 1;
-        mbar_wait(bar_kv_full + 8 * s, (j >> 1) & 1);
+        mbar_wait(bar_k_full + 8 * s, (j >> 1) & 1);
         tc_fence_after();
         const uint32_t kb = sb + kOffK + s * 2 * kKVPanel;
 #pragma unroll
@@ -244,10 +271,12 @@ __global__ void __launch_bounds__(kThreads, 2)
           umma(tmem + s * kBN, da, db, idS, kk > 0);
         }
         umma_commit(bar_s_full + 8 * s);
+        umma_commit(bar_k_empty + 8 * s);
       };
       issue_s(0);
       for (int j = 0; j < T; ++j) {
         if (j + 1 < T) issue_s(j + 1);
+        mbar_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
         mbar_wait(bar_p_full, j & 1);
         tc_fence_after();
         const uint32_t vb = sb + kOffV + (j & 1) * 2 * kKVPanel;
@@ -260,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           umma(tmem + 2 * kBN, da, db, idO, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(bar_o_done);
-        umma_commit(bar_kv_empty + 8 * (j & 1));
+        umma_commit(bar_v_empty + 8 * (j & 1));
       }
     }
   } else {
@@ -273,6 +302,43 @@ __global__ void __launch_bounds__(kThreads, 2)
     float raw_max = -INFINITY; // true maximum of the raw dot products
     float l = 0.f;
     uint8_t* prow = smem + kOffP + r * 128;
+    const int bl = r / a.G, g = r % a.G;
+    const int b = mt * (kBM / a.G) + bl;
+    const bool row_ok = b < a.bw;
+    const int h = kvh * a.G + g;
+    const int64_t qrow = (((int64_t)req * a.bw + b) * a.hq + h);
+    constexpr int kMaxU = 8;
+    const int nu = kPartial ? 0 : a.n_unshared;
+    float tu[kMaxU];   // unshared logits (log2 domain), computed while the first S tile is in flight
+#pragma unroll
+    for (int t = 0; t < kMaxU; ++t) tu[t] = -INFINITY;
+    if (!kPartial && nu > 0) {
+      mbar_wait(bar_q, 0);
+      if (row_ok) {
+        const __nv_bfloat16* kub = a.ku + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
+#pragma unroll 1
+        for (int t = 0; t < nu; ++t) {
+          const uint4* kr = reinterpret_cast<const uint4*>(kub + ((int64_t)t * a.hkv + kvh) * kD);
+          uint4 kv[16];
+#pragma unroll
+          for (int ch = 0; ch < 16; ++ch) kv[ch] = __ldg(kr + ch);
+          float dot[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int ch = 0; ch < 16; ++ch) {
+            const uint4 qv = *reinterpret_cast<const uint4*>(smem + kOffQ + (ch >> 3) * kQPanel + r * 128 +
+                                                             (((ch & 7) ^ (r & 7)) << 4));
+            float qf[8], kf[8];
+            bf16x8_to_f32(qv, qf);
+            bf16x8_to_f32(kv[ch], kf);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) dot[ch & 3] = fmaf(qf[e], kf[e], dot[ch & 3]);
+          }
+#pragma unroll
+          for (int u = 0; u < kMaxU; ++u)
+            if (u == t) tu[u] = ((dot[0] + dot[1]) + (dot[2] + dot[3])) * c2;
+        }
+      }
+    }
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
       mbar_wait(bar_s_full + 8 * s, (j >> 1) & 1);
@@ -293,9 +359,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int c = 0; c < 64; ++c)
           if (c >= valid) x[c] = -INFINITY;
       }
-      float tmax = x[0];
+      float mx[8];
 #pragma unroll
-      for (int c = 1; c < 64; ++c) tmax = fmaxf(tmax, x[c]);
+      for (int c = 0; c < 8; ++c) mx[c] = fmaxf(fmaxf(fmaxf(x[c], x[c + 8]), fmaxf(x[c + 16], x[c + 24])),
+                                               fmaxf(fmaxf(x[c + 32], x[c + 40]), fmaxf(x[c + 48], x[c + 56])));
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       raw_max = fmaxf(raw_max, tmax);
       const float t2 = tmax * c2;
       float alpha = 1.f;
@@ -306,15 +374,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         l *= alpha;
       }
       uint32_t pk[32];
-      float lsum = 0.f;
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int c = 0; c < 32; ++c) {
         const float p0 = ex2(fmaf(x[2 * c], c2, -m_ref));
         const float p1 = ex2(fmaf(x[2 * c + 1], c2, -m_ref));
-        lsum += p0 + p1;
+        ls4[c & 3] += p0 + p1;
         pk[c] = pack_bf16(p0, p1);
       }
-      l += lsum;
+      l += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       if (j > 0) {
         mbar_wait(bar_o_done, (j - 1) & 1);   // PV_{j-1} done: P buffer free, O stable
         tc_fence_after();
@@ -345,11 +413,6 @@ __global__ void __launch_bounds__(kThreads, 2)
       tc_fence_after();
     }
     // ---- epilogue ----
-    const int bl = r / a.G, g = r % a.G;
-    const int b = mt * (kBM / a.G) + bl;
-    const bool row_ok = b < a.bw;
-    const int h = kvh * a.G + g;
-    const int64_t qrow = (((int64_t)req * a.bw + b) * a.hq + h);
     const float t_true = raw_max * c2;
     if constexpr (kPartial) {
       const float f = (T > 0) ? ex2(m_ref - t_true) : 0.f;   // renormalise to the true maximum
@@ -376,35 +439,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     } else {
-      // unshared stage for this row (beam b's own tokens t < n_unshared) + merge
-      constexpr int kMaxU = 8;
-      float tu[kMaxU];
+      // merge with the unshared stage (beam b's own tokens t < n_unshared)
       float m_tot = (T > 0) ? m_ref : -INFINITY;
-      const int nu = a.n_unshared;
-      const __nv_bfloat16* kub = a.ku + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
-      const __nv_bfloat16* vub = a.vu + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
-      mbar_wait(bar_q, 0);   // the q rows are read from the Q tile (T == 0: nothing else waited)
       if (row_ok) {
 #pragma unroll
-        for (int t = 0; t < kMaxU; ++t) {
-          if (t < nu) {
-            const uint4* kr = reinterpret_cast<const uint4*>(kub + ((int64_t)t * a.hkv + kvh) * kD);
-            float dot = 0.f;
-#pragma unroll 4
-            for (int ch = 0; ch < 16; ++ch) {
-              const uint4 qv =
-                  *reinterpret_cast<const uint4*>(smem + kOffQ + (ch >> 3) * kQPanel + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
-              float qf[8], kf[8];
-              bf16x8_to_f32(qv, qf);
-              bf16x8_to_f32(__ldg(kr + ch), kf);
-#pragma unroll
-              for (int e = 0; e < 8; ++e) dot = fmaf(qf[e], kf[e], dot);
-            }
-            tu[t] = dot * c2;
-            m_tot = fmaxf(m_tot, tu[t]);
-          }
-        }
+        for (int t = 0; t < kMaxU; ++t) m_tot = fmaxf(m_tot, tu[t]);
       }
+      const __nv_bfloat16* vub = a.vu + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
+      const uint8_t* vus = smem + kOffK + bl * (nu * 256 + 16);
+      if (a.vu_smem && nu > 0) mbar_wait(bar_vu, 0);
       const float w_sh = (T > 0) ? ex2(m_ref - m_tot) : 0.f;
       float den = l * w_sh;
       float wu[kMaxU];
@@ -431,11 +474,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int t = 0; t < kMaxU; ++t) {
             if (t < nu) {
-              const uint4* vr = reinterpret_cast<const uint4*>(vub + ((int64_t)t * a.hkv + kvh) * kD + 32 * k);
+              const uint4* vr = a.vu_smem ? reinterpret_cast<const uint4*>(vus + t * 256 + 64 * k)
+                                          : reinterpret_cast<const uint4*>(vub + ((int64_t)t * a.hkv + kvh) * kD + 32 * k);
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
                 float vf[8];
-                bf16x8_to_f32(__ldg(vr + ch), vf);
+                bf16x8_to_f32(a.vu_smem ? vr[ch] : __ldg(vr + ch), vf);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[8 * ch + e] = fmaf(wu[t], vf[e], acc[8 * ch + e]);
               }
@@ -591,6 +635,7 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
   a.u_req_stride = u_req_stride; a.u_beam_stride = u_beam_stride;
   a.out = static_cast<__nv_bfloat16*>(out); a.lse = lse;
   a.pm = pm; a.ps = ps; a.po = po;
+  a.vu_smem = (!pm && n_unshared > 0 && (kBM / G) * (n_unshared * 256 + 16) <= (int)(2 * 2 * kKVPanel)) ? 1 : 0;
   const dim3 grid((unsigned)((bw * G + kBM - 1) / kBM), (unsigned)hkv, (unsigned)n_req);
   if (pm) {
     cudaFuncSetAttribute(k_attn_shared<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);

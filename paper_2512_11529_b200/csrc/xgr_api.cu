@@ -73,6 +73,13 @@ struct xgr_ctx {
 };
 static constexpr int kTimingRing = 4096;
 
+namespace xgr {
+bool pdl_enabled() {
+  static const bool on = !(getenv("XGR_PDL") && atoi(getenv("XGR_PDL")) == 0);
+  return on;
+}
+}  // namespace xgr
+
 static thread_local std::string g_err;
 
 static xgr_status fail(xgr_status st, const char* fmt, ...) {

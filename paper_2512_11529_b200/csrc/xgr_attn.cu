@@ -13,10 +13,13 @@
 //    operands in shared memory, fp32 accumulators in TMEM). Every KV tile is loaded once per
 //    128 query rows (the shared-prefix reuse of PAPER.md L224's "Ideal" curve) by TMA with the
 //    128-byte swizzle the MMA descriptors expect.
-//  * Warp roles per CTA (192 threads, 2 CTAs per SM): warp 0 = TMA producer (Q once, then a
-//    2-stage K/V ring), warp 1 = MMA issuer (one elected lane; S_{j+1} is issued before PV_j so
-//    the tensor core overlaps the softmax of tile j), warps 2-5 = softmax / correction /
-//    epilogue, thread <-> query row <-> TMEM lane. Online softmax in the log2 domain with a lazy
+//  * Warp roles per CTA (192 threads, 2 CTAs per SM): warp 0 = TMA producers (lane 0: Q once,
+//    then a 3-stage K ring whose stages are released right after their S MMA; lane 1: a 2-stage
+//    V ring released after the PV MMA), warp 1 = MMA issuer (one thread; S_{j+1} is issued before
+//    PV_j so the tensor core overlaps the softmax of tile j), warps 2-5 = softmax / correction /
+//    epilogue, thread <-> query row <-> TMEM lane. P is written back to TMEM over its own S tile
+//    (packed bf16 pairs) and read by the PV MMA as its A operand (tcgen05.mma with A in TMEM),
+//    so P never touches shared memory. Online softmax in the log2 domain with a lazy
 //    reference maximum: O (in TMEM) is rescaled only when a tile's maximum exceeds the reference
 //    by more than 8 (so p <= 2^8); exact in real arithmetic, the partial is renormalised to the
 //    true maximum at the end.
@@ -31,6 +34,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "xgr_internal.cuh"
 
@@ -44,10 +48,11 @@ constexpr int kThreads = 192;     // producer warp, MMA warp, 4 softmax warps
 constexpr uint32_t kQPanel = kBM * 128;        // 16 KB: 128 rows x 64 bf16
 constexpr uint32_t kKVPanel = kBN * 128;       // 8 KB: 64 keys x 64 bf16
 constexpr uint32_t kOffQ = 0;
-constexpr uint32_t kOffK = kOffQ + 2 * kQPanel;            // [stage][panel]
-constexpr uint32_t kOffV = kOffK + 2 * 2 * kKVPanel;
-constexpr uint32_t kOffP = kOffV + 2 * 2 * kKVPanel;       // 128 rows x 64 bf16 (one panel)
-constexpr uint32_t kOffBar = kOffP + kBM * 128;
+constexpr int kKStages = 3;      // K ring (released right after its S MMA)
+constexpr int kVStages = 2;      // V ring (released after its PV MMA)
+constexpr uint32_t kOffK = kOffQ + 2 * kQPanel;                  // [stage][panel]
+constexpr uint32_t kOffV = kOffK + kKStages * 2 * kKVPanel;
+constexpr uint32_t kOffBar = kOffV + kVStages * 2 * kKVPanel;   // P lives in TMEM (aliasing S)
 constexpr uint32_t kSmem = kOffBar + 256;
 constexpr uint32_t kTmemCols = 256;            // S0 [0,64), S1 [64,128), O [128,256)
 constexpr float kRescaleThreshold = 8.0f;      // log2 domain
@@ -70,6 +75,20 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
       "@!p bra WAIT_%=;\n}" ::"r"(b),
       "r"(parity)
       : "memory");
+}
+// Spin with a short sleep between polls (for the single-thread producer / MMA roles, so their
+// polling does not take issue slots from the softmax warps).
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok) : "r"(b), "r"(parity) : "memory");
+  while (!ok) {
+    __nanosleep(20);
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok) : "r"(b), "r"(parity) : "memory");
+  }
 }
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
                                             int c2, int c3) {
@@ -99,6 +118,13 @@ __device__ __forceinline__ void umma(uint32_t d_tmem, uint64_t a, uint64_t b, ui
       "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+// A operand from TMEM (kind::f16: M rows in the 128 lanes, K-major packed 16-bit pairs).
+__device__ __forceinline__ void umma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc));
 }
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
@@ -164,7 +190,7 @@ struct AttnArgs {
   float* pm;                         // partial mode: [n_req][bw][hq] m, s and [..][d] o (fp32)
   float* ps;
   float* po;
-  int vu_smem;                       // fused: stage the beams' unshared V rows in the K ring
+  int dbg;                           // XGR_ATTN_DBG (development experiments)
 };
 
 // grid: (ceil(bw*G/128), hkv, n_req); 192 threads; kSmem dynamic shared memory.
@@ -178,24 +204,27 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int T = (a.ls + kBN - 1) / kBN;
   const uint32_t sb = su32(smem);
   if (sb & 1023u) __trap();   // the 128-byte swizzle atoms need 1024-byte alignment
-  // barriers: Q; K ring full/empty [2]; V ring full/empty [2]; S full [2]; P full; O done
-  const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 24,
-                 bar_v_full = bar_q + 40, bar_v_empty = bar_q + 56, bar_s_full = bar_q + 72,
-                 bar_p_full = bar_q + 88, bar_o_done = bar_q + 96, bar_vu = bar_q + 104;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 128);
+  // barriers: Q; K ring full/empty [3]; V ring full/empty [2]; S full [2]; P full; O done; O final
+  const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 32,
+                 bar_v_full = bar_q + 56, bar_v_empty = bar_q + 72, bar_s_full = bar_q + 88,
+                 bar_p_full = bar_q + 104, bar_o_done = bar_q + 112,
+                 bar_o_final = bar_q + 120;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 192);
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
       mbar_init(bar_k_full + 8 * i, 1);
       mbar_init(bar_k_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(bar_v_full + 8 * i, 1);
       mbar_init(bar_v_empty + 8 * i, 1);
       mbar_init(bar_s_full + 8 * i, 1);
     }
     mbar_init(bar_p_full, 128);
     mbar_init(bar_o_done, 1);
-    mbar_init(bar_vu, 1);
+    mbar_init(bar_o_final, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm_q);
     prefetch_map(&tm_k);
@@ -211,6 +240,9 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  auto role_wait = [&](uint32_t b, uint32_t par) {
+    if (a.dbg & 4) mbar_wait_sleep(b, par); else mbar_wait(b, par);
+  };
   if (warp == 0) {
     // ===== TMA producers: lane 0 streams Q then K, lane 1 streams V. A K stage is released by the
     // commit after its S MMA, a V stage after its PV MMA, so K_{j+2} is in flight while tile j's
@@ -226,30 +258,14 @@ __global__ void __launch_bounds__(kThreads, 2)
       const uint32_t full0 = lane == 0 ? bar_k_full : bar_v_full;
       const uint32_t empty0 = lane == 0 ? bar_k_empty : bar_v_empty;
       const uint32_t buf0 = sb + (lane == 0 ? kOffK : kOffV);
+      const int ns = lane == 0 ? kKStages : kVStages;
       for (int j = 0; j < T; ++j) {
-        const int s = j & 1, u = j >> 1;
-        if (j >= 2) mbar_wait(empty0 + 8 * s, (u + 1) & 1);
+        const int s = j % ns, u = j / ns;
+        if (j >= ns) role_wait(empty0 + 8 * s, (u + 1) & 1);
         const uint32_t full = full0 + 8 * s, dst = buf0 + s * 2 * kKVPanel;
         mbar_expect_tx(full, 2 * kKVPanel);
         tma_load_4d(dst, tm, full, 0, kvh, j * kBN, req);
         tma_load_4d(dst + kKVPanel, tm, full, 64, kvh, j * kBN, req);
-      }
-      if (!kPartial && lane == 0 && a.vu_smem) {
-        // the epilogue's unshared V rows, staged in the K ring once its last tiles are consumed
-        for (int j = max(0, T - 2); j < T; ++j) mbar_wait(bar_k_empty + 8 * (j & 1), (j >> 1) & 1);
-        const int nb = kBM / a.G, b0 = mt * nb, nbv = min(nb, a.bw - b0), nu = a.n_unshared;
-        const uint32_t rs = (uint32_t)nu * 256 + 16;
-        mbar_expect_tx(bar_vu, (uint32_t)(nbv * nu * 256));
-        for (int bl = 0; bl < nbv; ++bl)
-          for (int t = 0; t < nu; ++t) {
-            const __nv_bfloat16* src = a.vu + (int64_t)req * a.u_req_stride + (int64_t)(b0 + bl) * a.u_beam_stride +
-                                       ((int64_t)t * a.hkv + kvh) * kD;
-            asm volatile(
-                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 256, [%2];" ::"r"(
-                    sb + kOffK + bl * rs + t * 256),
-                "l"(src), "r"(bar_vu)
-                : "memory");
-          }
       }
     }
   } else if (warp == 1) {
@@ -257,12 +273,12 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0 && T > 0) {
       constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0);
       constexpr uint32_t idO = idesc_bf16(kBM, kD, 1);
-      mbar_wait(bar_q, 0);
+      role_wait(bar_q, 0);
       auto issue_s = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(bar_k_full + 8 * s, (j >> 1) & 1);
+        const int s = j & 1, ks = j % kKStages;
+        role_wait(bar_k_full + 8 * ks, (j / kKStages) & 1);
         tc_fence_after();
-        const uint32_t kb = sb + kOffK + s * 2 * kKVPanel;
+        const uint32_t kb = sb + kOffK + ks * 2 * kKVPanel;
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk) {
           const uint32_t p = kk >> 2, off = (kk & 3) * 32;
@@ -271,26 +287,27 @@ __global__ void __launch_bounds__(kThreads, 2)
           umma(tmem + s * kBN, da, db, idS, kk > 0);
         }
         umma_commit(bar_s_full + 8 * s);
-        umma_commit(bar_k_empty + 8 * s);
+        umma_commit(bar_k_empty + 8 * ks);
       };
       issue_s(0);
       for (int j = 0; j < T; ++j) {
         if (j + 1 < T) issue_s(j + 1);
-        mbar_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
-        mbar_wait(bar_p_full, j & 1);
+        role_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
+        role_wait(bar_p_full, j & 1);
         tc_fence_after();
         const uint32_t vb = sb + kOffV + (j & 1) * 2 * kKVPanel;
 #pragma unroll
         for (int kk = 0; kk < kBN / 16; ++kk) {
-          const uint64_t da = sdesc(sb + kOffP + kk * 32, 16, 1024);
-          // V tile, MN-major: 64-element d panels at LBO = 8 KB, 8-key groups at SBO = 1 KB,
-          // 16 keys per MMA = 2 KB.
+          // A = P_j from TMEM (packed bf16 pairs in the first 32 columns of S buffer j % 2,
+          // 8 columns per 16 keys); B = V tile, MN-major: 64-element d panels at LBO = 8 KB,
+          // 8-key groups at SBO = 1 KB, 16 keys per MMA = 2 KB.
           const uint64_t db = sdesc(vb + kk * 2048, kKVPanel, 1024);
-          umma(tmem + 2 * kBN, da, db, idO, (j > 0 || kk > 0) ? 1u : 0u);
+          umma_ts(tmem + 2 * kBN, tmem + (j & 1) * kBN + kk * 8, db, idO, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(bar_o_done);
         umma_commit(bar_v_empty + 8 * (j & 1));
       }
+      umma_commit(bar_o_final);   // a one-phase barrier: the epilogue may skip o_done phases
     }
   } else {
     // ===== softmax / correction / epilogue: thread <-> query row <-> TMEM lane =====
@@ -301,7 +318,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     float m_ref = -INFINITY;   // reference maximum (log2 domain) that O and l are relative to
     float raw_max = -INFINITY; // true maximum of the raw dot products
     float l = 0.f;
-    uint8_t* prow = smem + kOffP + r * 128;
     const int bl = r / a.G, g = r % a.G;
     const int b = mt * (kBM / a.G) + bl;
     const bool row_ok = b < a.bw;
@@ -383,33 +399,32 @@ __global__ void __launch_bounds__(kThreads, 2)
         pk[c] = pack_bf16(p0, p1);
       }
       l += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      // P_j -> TMEM over S_j (the PV MMA reads it as its A operand); the S buffer is rewritten
+      // only by S_{j+2}, issued after PV_j
       if (j > 0) {
-        mbar_wait(bar_o_done, (j - 1) & 1);   // PV_{j-1} done: P buffer free, O stable
+        // PV_{j-1} done before P_j is written (a lazy variant that skipped this wait when no
+        // correction was needed raced intermittently; measured no faster) and before O is rescaled
+        mbar_wait(bar_o_done, (j - 1) & 1);
         tc_fence_after();
-        if (__any_sync(0xffffffffu, resc)) {
+      }
+      tmem_st32(tmem + lane_base + s * kBN, pk);
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t o[32];
-            tmem_ld32(tmem + lane_base + 2 * kBN + 32 * k, o);
-            tmem_wait_ld();
+        for (int k = 0; k < 4; ++k) {
+          uint32_t o[32];
+          tmem_ld32(tmem + lane_base + 2 * kBN + 32 * k, o);
+          tmem_wait_ld();
 #pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
-            tmem_st32(tmem + lane_base + 2 * kBN + 32 * k, o);
-          }
-          tmem_wait_st();
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          tmem_st32(tmem + lane_base + 2 * kBN + 32 * k, o);
         }
       }
-#pragma unroll
-      for (int ch = 0; ch < 8; ++ch) {
-        const uint4 v = make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (r & 7)) << 4)) = v;
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar_p_full);
     }
     if (T > 0) {
-      mbar_wait(bar_o_done, (T - 1) & 1);
+      mbar_wait(bar_o_final, 0);
       tc_fence_after();
     }
     // ---- epilogue ----
@@ -446,8 +461,6 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int t = 0; t < kMaxU; ++t) m_tot = fmaxf(m_tot, tu[t]);
       }
       const __nv_bfloat16* vub = a.vu + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
-      const uint8_t* vus = smem + kOffK + bl * (nu * 256 + 16);
-      if (a.vu_smem && nu > 0) mbar_wait(bar_vu, 0);
       const float w_sh = (T > 0) ? ex2(m_ref - m_tot) : 0.f;
       float den = l * w_sh;
       float wu[kMaxU];
@@ -474,12 +487,11 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int t = 0; t < kMaxU; ++t) {
             if (t < nu) {
-              const uint4* vr = a.vu_smem ? reinterpret_cast<const uint4*>(vus + t * 256 + 64 * k)
-                                          : reinterpret_cast<const uint4*>(vub + ((int64_t)t * a.hkv + kvh) * kD + 32 * k);
+              const uint4* vr = reinterpret_cast<const uint4*>(vub + ((int64_t)t * a.hkv + kvh) * kD + 32 * k);
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
                 float vf[8];
-                bf16x8_to_f32(a.vu_smem ? vr[ch] : __ldg(vr + ch), vf);
+                bf16x8_to_f32(__ldg(vr + ch), vf);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[8 * ch + e] = fmaf(wu[t], vf[e], acc[8 * ch + e]);
               }
@@ -635,7 +647,8 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
   a.u_req_stride = u_req_stride; a.u_beam_stride = u_beam_stride;
   a.out = static_cast<__nv_bfloat16*>(out); a.lse = lse;
   a.pm = pm; a.ps = ps; a.po = po;
-  a.vu_smem = (!pm && n_unshared > 0 && (kBM / G) * (n_unshared * 256 + 16) <= (int)(2 * 2 * kKVPanel)) ? 1 : 0;
+  static const int dbg_env = getenv("XGR_ATTN_DBG") ? atoi(getenv("XGR_ATTN_DBG")) : 0;
+  a.dbg = dbg_env;
   const dim3 grid((unsigned)((bw * G + kBM - 1) / kBM), (unsigned)hkv, (unsigned)n_req);
   if (pm) {
     cudaFuncSetAttribute(k_attn_shared<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);

@@ -38,6 +38,8 @@ __global__ void __launch_bounds__(WPB * 32) k_head(const __grid_constant__ StepA
                                                    int64_t hreq, const __nv_bfloat16* __restrict__ head,
                                                    int64_t ldw, const float* __restrict__ bias, int d,
                                                    float* __restrict__ clog) {
+  pdl_wait();
+  pdl_trigger();
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * WPB + (threadIdx.x >> 5), req = blockIdx.y;
   if (b >= a.BW) return;
@@ -87,9 +89,9 @@ cudaError_t launch_head(const StepArgs& a, const void* hidden, int64_t ldh, int6
   static const int kc = getenv("XGR_HEAD_KC") ? atoi(getenv("XGR_HEAD_KC")) : 4;
   const __nv_bfloat16* h = static_cast<const __nv_bfloat16*>(hidden);
   const __nv_bfloat16* w = static_cast<const __nv_bfloat16*>(head);
-  if (kc == 8) k_head<WPB, 8><<<grid, WPB * 32, 0, s>>>(a, h, ldh, hreq, w, ldw, bias, d, clog);
-  else if (kc == 2) k_head<WPB, 2><<<grid, WPB * 32, 0, s>>>(a, h, ldh, hreq, w, ldw, bias, d, clog);
-  else k_head<WPB, 4><<<grid, WPB * 32, 0, s>>>(a, h, ldh, hreq, w, ldw, bias, d, clog);
+  if (kc == 8) launch_pdl(k_head<WPB, 8>, grid, WPB * 32, 0, s, a, h, ldh, hreq, w, ldw, bias, d, clog);
+  else if (kc == 2) launch_pdl(k_head<WPB, 2>, grid, WPB * 32, 0, s, a, h, ldh, hreq, w, ldw, bias, d, clog);
+  else launch_pdl(k_head<WPB, 4>, grid, WPB * 32, 0, s, a, h, ldh, hreq, w, ldw, bias, d, clog);
   return cudaGetLastError();
 }
 

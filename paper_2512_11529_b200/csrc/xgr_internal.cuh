@@ -6,10 +6,37 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 
 #include "../../include/xgr_beam.h"
 
 namespace xgr {
+
+// ---- programmatic dependent launch (PDL) ----------------------------------------------------
+// Step kernels are launched with programmatic stream serialization: a kernel's CTAs may be
+// scheduled while its stream predecessor drains. Every such kernel executes pdl_wait() (wait for
+// the predecessor grid to complete and its writes to be visible) before touching global memory,
+// and pdl_trigger() early so its own successor can be scheduled. XGR_PDL=0 disables it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 constexpr int kMaxND = 8;
 constexpr int kMaxBW = 1024;

@@ -575,6 +575,8 @@ __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, c
 // ---------------------------------------------------------------------------------------------
 template <int T, int VPT>
 __global__ void __launch_bounds__(T) k_theta(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_bm[T * VPT / 8];
   __shared__ float s_red[T / 32], s_red2[T / 32], s_red3[T / 32];
   __shared__ uint32_t s_hist[4096];
@@ -724,6 +726,8 @@ __device__ void sparse_row_main(const StepArgs& a, int req, int b, float S, floa
 
 template <int T, int VPT>
 __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ uint32_t s_bm[T * VPT / 8];
   __shared__ float s_red[T / 32], s_red2[T / 32];
   __shared__ int s_redi[T / 32];
@@ -938,6 +942,8 @@ __device__ void topk_scan(const uint64_t* keys, int m, int K, int V, int BW, int
 
 template <int T, typename TI = float>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
   uint64_t* s_cand = s_keys + a.cap;
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
@@ -1043,6 +1049,8 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
 template <int T>
 __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a, const uint64_t* grec,
                                              const int32_t* grec_n) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint64_t s_keys[];  // [nranks * BW] keys, then [2 * kMaxBW]
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ TopkScratch s_sc;
@@ -1080,6 +1088,8 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
 // ---------------------------------------------------------------------------------------------
 template <int T, bool ROOT, typename TI = float, bool CMP = false>
 __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
   uint64_t* s_cand = s_dynk;
   uint64_t* s_keys = s_dynk + 2 * kMaxBW;
@@ -1405,12 +1415,12 @@ static cudaError_t launch_dense(const StepArgs& a, int rows, cudaStream_t s, cud
   if (!a.no_prune && !a.topk) {   // a single row's bound is no bound for the per-beam Top-K pool
     int r0 = min(a.theta_rows, rows);
     if (r0 > 0) {
-      k_theta<T, VPT><<<dim3(a.batch, r0), T, 0, s>>>(a);
+      launch_pdl(k_theta<T, VPT>, dim3(a.batch, r0), T, 0, s, a);
       ++*launches;
     }
   }
   if (ev0) cudaEventRecord(ev0, s);
-  k_main<T, VPT><<<dim3(a.batch, rows), T, 0, s>>>(a);
+  launch_pdl(k_main<T, VPT>, dim3(a.batch, rows), T, 0, s, a);
   ++*launches;
   if (ev1) cudaEventRecord(ev1, s);
   return cudaGetLastError();
@@ -1447,11 +1457,11 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   if (sparse_route) {
     size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
     if (bf16) {
-      if (rows == 1) k_sparse<512, true, __nv_bfloat16><<<a.batch, 512, smem, s>>>(a);
-      else k_sparse<512, false, __nv_bfloat16><<<a.batch, 512, smem, s>>>(a);
+      if (rows == 1) launch_pdl(k_sparse<512, true, __nv_bfloat16>, a.batch, 512, smem, s, a);
+      else launch_pdl(k_sparse<512, false, __nv_bfloat16>, a.batch, 512, smem, s, a);
     } else {
-      if (rows == 1) k_sparse<512, true><<<a.batch, 512, smem, s>>>(a);
-      else k_sparse<512, false><<<a.batch, 512, smem, s>>>(a);
+      if (rows == 1) launch_pdl(k_sparse<512, true>, a.batch, 512, smem, s, a);
+      else launch_pdl(k_sparse<512, false>, a.batch, 512, smem, s, a);
     }
     ++*launches;
     return cudaGetLastError();
@@ -1471,8 +1481,8 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   else return cudaErrorNotSupported;
   if (e != cudaSuccess) return e;
   const size_t sel = ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t);
-  if (bf16) k_select<512, __nv_bfloat16><<<a.batch, 512, sel, s>>>(a);
-  else k_select<512><<<a.batch, 512, sel, s>>>(a);
+  if (bf16) launch_pdl(k_select<512, __nv_bfloat16>, a.batch, 512, sel, s, a);
+  else launch_pdl(k_select<512>, a.batch, 512, sel, s, a);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -1480,7 +1490,7 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
 // LM-head fusion (NEXT f4): the sparse step over the compact legal logits a.clog written by k_head.
 cudaError_t launch_sparse_compact(const StepArgs& a, int sparse_keys, cudaStream_t s, int* launches) {
   const size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
-  k_sparse<512, false, float, true><<<a.batch, 512, smem, s>>>(a);
+  launch_pdl(k_sparse<512, false, float, true>, a.batch, 512, smem, s, a);
   ++*launches;
   return cudaGetLastError();
 }
@@ -1494,7 +1504,7 @@ cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s);
 cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches) {
   cudaError_t e = launch_shard_emit(a, rows, s);
   if (e != cudaSuccess) return e;
-  k_select<512><<<a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s>>>(a);
+  launch_pdl(k_select<512>, a.batch, 512, ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t), s, a);
   *launches += 3;
   return cudaGetLastError();
 }
@@ -1504,7 +1514,7 @@ cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const in
   const size_t smem = ((size_t)a.nranks * a.BW + 2 * kMaxBW) * sizeof(uint64_t);
   cudaError_t e = cudaFuncSetAttribute(k_merge<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_merge<512><<<a.batch, 512, smem, s>>>(a, grec, grec_n);
+  launch_pdl(k_merge<512>, a.batch, 512, smem, s, a, grec, grec_n);
   return cudaGetLastError();
 }
 

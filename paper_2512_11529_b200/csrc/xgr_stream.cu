@@ -162,6 +162,8 @@ __device__ __forceinline__ int cisum(int v, int* part) {
 // ------------------------------------------------------------------------------------------
 template <int CTR, int R0, int MODE = kModeNormal>
 __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NT = CTR * R0;
   extern __shared__ __align__(128) float s_dyn[];
   float* s_row = s_dyn;                                                   // [R0][32*CTR]
@@ -492,6 +494,8 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 // ------------------------------------------------------------------------------------------
 template <int T, int NCH, typename TI = float>
 __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk
   constexpr int VPT = NCH * CH / 4;          // x[] holds 4 * VPT = NCH * CH tokens per thread
   constexpr int NW = T / 32;
@@ -638,6 +642,8 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
 
 template <int T>
 __global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int PER = kSeedBins / T;
   __shared__ uint32_t s_w[T / 32];
   __shared__ int s_bin;
@@ -705,6 +711,8 @@ __device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
 template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float>
 __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int GT = 256;          // consumer threads per group
   constexpr int VT = GT * EPT;     // tokens per stage row
   constexpr int MW = VT / 32;      // mask words per stage
@@ -1238,15 +1246,15 @@ cudaError_t configure_stream_kernels() {
 cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s) {
   const int total = a.batch * rows;
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
-  k_stream<32, 1, 2, 3, kModeStats><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 0);
+  launch_pdl(k_stream<32, 1, 2, 3, kModeStats>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, 0);
   return cudaGetLastError();
 }
 
 cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s) {
   const int total = a.batch * rows;
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
-  k_seed<256, 4, kModeShardEmit><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
-  k_stream<32, 1, 2, 3, kModeShardEmit><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, 4);
+  launch_pdl(k_seed<256, 4, kModeShardEmit>, a.batch, 1024, stream_smem<32, 4>(), s, a);
+  launch_pdl(k_stream<32, 1, 2, 3, kModeShardEmit>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, 4);
   return cudaGetLastError();
 }
 
@@ -1266,19 +1274,19 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     if (r0 > 0) {
       const int ns = a.batch * r0;
       if (a.trie.V <= 8192 && g_seed_kernel != 1 && !a.topk)
-        k_stream<32, 1, 4, 3, kModeSeedHist, bf><<<std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s>>>(
+        launch_pdl(k_stream<32, 1, 4, 3, kModeSeedHist, bf>, std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s, 
             a, ns, 0);
-      else if (a.trie.V <= 8192) k_seed_hist<256, 4, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
-      else k_seed_hist<256, 8, bf><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      else if (a.trie.V <= 8192) launch_pdl(k_seed_hist<256, 4, bf>, dim3(a.batch, r0), 256, 0, s, a);
+      else launch_pdl(k_seed_hist<256, 8, bf>, dim3(a.batch, r0), 256, 0, s, a);
       ++*launches;
     }
-    k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+    launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     if (ev0) cudaEventRecord(ev0, s);
     if (a.trie.V <= 8192)
-      k_stream<32, 1, 4, 3, kModeNormal, bf><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s>>>(
+      launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s, 
           a, total, 0);
     else
-      k_stream<64, 1, 3, 2, kModeNormal, bf><<<std::min(total, 2 * sms), 256 + 32, stream_smem<64, 3, bf>(), s>>>(
+      launch_pdl(k_stream<64, 1, 3, 2, kModeNormal, bf>, std::min(total, 2 * sms), 256 + 32, stream_smem<64, 3, bf>(), s, 
           a, total, 0);
     if (ev1) cudaEventRecord(ev1, s);
     *launches += 2;
@@ -1290,44 +1298,44 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       const int r0 = std::min(a.theta_rows, rows);
       if (r0 > 0) {
         if (g_seed_kernel == 1 || a.topk) {   // one CTA per seed row (XGR_SEED_KERNEL=1; Top-K cap)
-          k_seed_hist<256, 8><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+          launch_pdl(k_seed_hist<256, 8>, dim3(a.batch, r0), 256, 0, s, a);
         } else {                    // the seed rows streamed by the persistent kernel
           const int ns = a.batch * r0;
-          k_stream<32, 1, 2, 3, kModeSeedHist><<<std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, ns, 0);
+          launch_pdl(k_stream<32, 1, 2, 3, kModeSeedHist>, std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, ns, 0);
         }
         ++*launches;
       }
-      k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+      launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
       seeded = 0;
     } else if (seeded == 2) {
-      k_seed<256, 2><<<a.batch, 512, stream_smem<32, 2>(), s>>>(a);
+      launch_pdl(k_seed<256, 2>, a.batch, 512, stream_smem<32, 2>(), s, a);
     } else {
-      k_seed<256, 4><<<a.batch, 1024, stream_smem<32, 4>(), s>>>(a);
+      launch_pdl(k_seed<256, 4>, a.batch, 1024, stream_smem<32, 4>(), s, a);
     }
     if (ev0) cudaEventRecord(ev0, s);
     switch (g_stream_variant) {
       case 1:   // one CTA per SM: one producer feeding three consumer groups from a 6-stage ring
-        k_stream<32, 3, 6><<<grid, 3 * 256 + 32, stream_smem<32, 6>(), s>>>(a, total, seeded);
+        launch_pdl(k_stream<32, 3, 6>, grid, 3 * 256 + 32, stream_smem<32, 6>(), s, a, total, seeded);
         break;
       case 2:
-        k_stream<32, 1, 1, 4><<<std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s>>>(a, total, seeded);
+        launch_pdl(k_stream<32, 1, 1, 4>, std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s, a, total, seeded);
         break;
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
-        k_stream<32, 1, 2, 3><<<std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s>>>(a, total, seeded);
+        launch_pdl(k_stream<32, 1, 2, 3>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, seeded);
     }
   } else if (a.topk) {   // V > 8192 with per-beam Top-K: the capped histogram seed
     const int r0 = std::min(a.theta_rows, rows);
     if (r0 > 0) {
-      k_seed_hist<256, 16><<<dim3(a.batch, r0), 256, 0, s>>>(a);
+      launch_pdl(k_seed_hist<256, 16>, dim3(a.batch, r0), 256, 0, s, a);
       ++*launches;
     }
-    k_seed_theta<256><<<a.batch, 256, 0, s>>>(a);
+    launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     if (ev0) cudaEventRecord(ev0, s);
-    k_stream<64, 2, 3><<<grid, 2 * 256 + 32, stream_smem<64, 3>(), s>>>(a, total, 0);
+    launch_pdl(k_stream<64, 2, 3>, grid, 2 * 256 + 32, stream_smem<64, 3>(), s, a, total, 0);
   } else {
-    k_seed<512, 2><<<a.batch, 1024, stream_smem<64, 2>(), s>>>(a);
+    launch_pdl(k_seed<512, 2>, a.batch, 1024, stream_smem<64, 2>(), s, a);
     if (ev0) cudaEventRecord(ev0, s);
-    k_stream<64, 2, 3><<<grid, 2 * 256 + 32, stream_smem<64, 3>(), s>>>(a, total, 2);
+    launch_pdl(k_stream<64, 2, 3>, grid, 2 * 256 + 32, stream_smem<64, 3>(), s, a, total, 2);
   }
   if (ev1) cudaEventRecord(ev1, s);
   *launches += 2;

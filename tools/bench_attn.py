@@ -40,6 +40,7 @@ def main():
     c = ATTN_CONFIGS[cfg]
     n_req, bw, hq, hkv, d, ls, nd = (c[k] for k in ("n_req", "bw", "hq", "hkv", "d", "ls", "nd"))
     ls = int(os.environ.get("ATTN_LS", ls))
+    nu = int(os.environ.get("ATTN_NU", nd))
     scale = 1.0 / math.sqrt(d)
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
@@ -48,7 +49,7 @@ def main():
     ks, vs = rnd(n_req, ls, hkv, d), rnd(n_req, ls, hkv, d)
     ku, vu = rnd(n_req, bw, nd, hkv, d), rnd(n_req, bw, nd, hkv, d)
     out = torch.empty_like(q)
-    run = lambda: xgr.attn_staged(q, ks, vs, ku, vu, nd, hkv, scale, out=out)
+    run = lambda: xgr.attn_staged(q, ks, vs, ku, vu, nu, hkv, scale, out=out)
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -59,7 +60,7 @@ def main():
     ms_mean = sum(ts) / len(ts)
     rows = n_req * bw * hq
     flops = 4.0 * rows * ls * d
-    byts = (q.numel() + out.numel() + ks.numel() + vs.numel() + n_req * bw * nd * hkv * d * 2) * 2
+    byts = (q.numel() + out.numel() + ks.numel() + vs.numel() + n_req * bw * nu * hkv * d * 2) * 2
     per_beam_bytes = (q.numel() + out.numel()) * 2 + n_req * bw * (ls + nd) * hkv * d * 2 * 2
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -70,7 +71,7 @@ def main():
     tf = flops / (ms_mean / 1e3) / 1e12
     res = {"kernel": "k_attn_shared<false> (tcgen05 shared stage + fused unshared stage and merge)",
            "workload": cfg, "n_req": n_req, "bw": bw, "hq": hq, "hkv": hkv, "d": d, "ls": ls,
-           "n_unshared": nd, "ms_mean": ms_mean, "ms_p50": ms, "ms_all": ts,
+           "n_unshared": nu, "ms_mean": ms_mean, "ms_p50": ms, "ms_all": ts,
            "roofline": {"bound": "tensor", "achieved": tf, "peak": peak_tf, "unit": "TFLOP/s",
                         "frac": tf / peak_tf, "peak_source": src, "alg_flops": flops},
            "hbm": {"alg_bytes": byts, "achieved_gbs": byts / (ms_mean / 1e3) / 1e9, "peak_gbs": peak_bw,

@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 
 #include "xgr_internal.cuh"
 
@@ -97,6 +98,20 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "%6}], [%2];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, "
+      "%6, %7}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
@@ -191,13 +206,17 @@ struct AttnArgs {
   float* ps;
   float* po;
   int dbg;                           // XGR_ATTN_DBG (development experiments)
+  int u_stage;                       // fused: unshared K/V rows TMA-staged in the K ring
+  int o_tma;                         // fused: output tile written by TMA from the V ring
 };
 
 // grid: (ceil(bw*G/128), hkv, n_req); 192 threads; kSmem dynamic shared memory.
 template <bool kPartial>
 __global__ void __launch_bounds__(kThreads, 2)
     k_attn_shared(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                  const __grid_constant__ CUtensorMap tm_v, const AttnArgs a) {
+                  const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ku,
+                  const __grid_constant__ CUtensorMap tm_vu, const __grid_constant__ CUtensorMap tm_o,
+                  const AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
@@ -208,7 +227,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 32,
                  bar_v_full = bar_q + 56, bar_v_empty = bar_q + 72, bar_s_full = bar_q + 88,
                  bar_p_full = bar_q + 104, bar_o_done = bar_q + 112,
-                 bar_o_final = bar_q + 120;
+                 bar_o_final = bar_q + 120, bar_u = bar_q + 128;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 192);
 
   if (threadIdx.x == 0) {
@@ -225,6 +244,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(bar_p_full, 128);
     mbar_init(bar_o_done, 1);
     mbar_init(bar_o_final, 1);
+    mbar_init(bar_u, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     prefetch_map(&tm_q);
     prefetch_map(&tm_k);
@@ -266,6 +286,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_expect_tx(full, 2 * kKVPanel);
         tma_load_4d(dst, tm, full, 0, kvh, j * kBN, req);
         tma_load_4d(dst + kKVPanel, tm, full, 64, kvh, j * kBN, req);
+      }
+      if (!kPartial && lane == 0 && a.u_stage) {
+        // the CTA's beams' own K/V rows (beam-major, then token), one TMA box per 64-dim panel,
+        // into the K ring as soon as its last tiles have been consumed by their S MMAs
+        for (int j = max(0, T - kKStages); j < T; ++j)
+          role_wait(bar_k_empty + 8 * (j % kKStages), (j / kKStages) & 1);
+        const uint32_t pu = (uint32_t)(kBM / a.G) * a.n_unshared * 128;
+        const int b0 = mt * (kBM / a.G);
+        mbar_expect_tx(bar_u, 4 * pu);
+        tma_load_5d(sb + kOffK, &tm_ku, bar_u, 0, kvh, 0, b0, req);
+        tma_load_5d(sb + kOffK + pu, &tm_ku, bar_u, 64, kvh, 0, b0, req);
+        tma_load_5d(sb + kOffK + 2 * pu, &tm_vu, bar_u, 0, kvh, 0, b0, req);
+        tma_load_5d(sb + kOffK + 3 * pu, &tm_vu, bar_u, 64, kvh, 0, b0, req);
       }
     }
   } else if (warp == 1) {
@@ -328,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     float tu[kMaxU];   // unshared logits (log2 domain), computed while the first S tile is in flight
 #pragma unroll
     for (int t = 0; t < kMaxU; ++t) tu[t] = -INFINITY;
-    if (!kPartial && nu > 0) {
+    if (!kPartial && nu > 0 && !a.u_stage) {
       mbar_wait(bar_q, 0);
       if (row_ok) {
         const __nv_bfloat16* kub = a.ku + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
@@ -455,6 +488,33 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
     } else {
       // merge with the unshared stage (beam b's own tokens t < n_unshared)
+      const uint32_t pu = (uint32_t)(kBM / a.G) * nu * 128;   // staged panel bytes
+      auto urow = [&](int panel, int t, int ch) -> uint4 {     // staged unshared row (bl, t), 16-B chunk
+        const int R = bl * nu + t;
+        return *reinterpret_cast<const uint4*>(smem + kOffK + panel * pu + R * 128 + (((ch & 7) ^ (R & 7)) << 4));
+      };
+      if (a.u_stage) {
+        mbar_wait(bar_u, 0);
+        if (row_ok) {
+#pragma unroll 1
+          for (int t = 0; t < nu; ++t) {
+            float dot[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int ch = 0; ch < 16; ++ch) {
+              const uint4 qv = *reinterpret_cast<const uint4*>(smem + kOffQ + (ch >> 3) * kQPanel + r * 128 +
+                                                               (((ch & 7) ^ (r & 7)) << 4));
+              float qf[8], kf[8];
+              bf16x8_to_f32(qv, qf);
+              bf16x8_to_f32(urow(ch >> 3, t, ch), kf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) dot[ch & 3] = fmaf(qf[e], kf[e], dot[ch & 3]);
+            }
+#pragma unroll
+            for (int u = 0; u < kMaxU; ++u)
+              if (u == t) tu[u] = ((dot[0] + dot[1]) + (dot[2] + dot[3])) * c2;
+          }
+        }
+      }
       float m_tot = (T > 0) ? m_ref : -INFINITY;
       if (row_ok) {
 #pragma unroll
@@ -480,10 +540,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
           for (int c = 0; c < 32; ++c) o[c] = 0u;
         }
-        if (row_ok) {
-          float acc[32];
+        float acc[32];
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(o[c]) * w_sh;
+        for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(o[c]) * w_sh;
+        if (row_ok) {
 #pragma unroll
           for (int t = 0; t < kMaxU; ++t) {
             if (t < nu) {
@@ -491,19 +551,42 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
               for (int ch = 0; ch < 4; ++ch) {
                 float vf[8];
-                bf16x8_to_f32(__ldg(vr + ch), vf);
+                bf16x8_to_f32(a.u_stage ? urow(2 + (k >> 1), t, (k & 1) * 4 + ch) : __ldg(vr + ch), vf);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[8 * ch + e] = fmaf(wu[t], vf[e], acc[8 * ch + e]);
               }
             }
           }
+        }
+        uint4 pk4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          pk4[c] = make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
+                              pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
+                              pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
+                              pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+        if (a.o_tma) {
+          // the output tile in the V ring (free: every PV MMA is complete), in the swizzled layout
+          // of the output tensor map's box (row r, 64-dim panels)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int ch = (k & 1) * 4 + c;
+            *reinterpret_cast<uint4*>(smem + kOffV + (k >> 1) * kQPanel + r * 128 + ((ch ^ (r & 7)) << 4)) = pk4[c];
+          }
+        } else if (row_ok) {
           uint4* dst = reinterpret_cast<uint4*>(a.out + qrow * kD + 32 * k);
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            dst[c] = make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
-                                pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
-                                pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
-                                pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+          for (int c = 0; c < 4; ++c) dst[c] = pk4[c];
+        }
+      }
+      if (a.o_tma) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 softmax warps
+        if (r == 0) {
+          tma_store_4d(&tm_o, sb + kOffV, 0, kvh * a.G, mt * (kBM / a.G), req);
+          tma_store_4d(&tm_o, sb + kOffV + kQPanel, 64, kvh * a.G, mt * (kBM / a.G), req);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem read before exit
         }
       }
       if (row_ok && a.lse) a.lse[qrow] = (m_tot + __log2f(den)) * 0.6931471805599453f;
@@ -605,6 +688,18 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// N-D bf16 map (N = 4 or 5), dims innermost first, 128-byte swizzle, box inner = 64 elements.
+static bool make_map_nd(CUtensorMap* m, const void* base, int rank, const uint64_t* dims, const uint64_t* strides_bytes,
+                        const uint32_t* box) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base),
+                        reinterpret_cast<const cuuint64_t*>(dims), reinterpret_cast<const cuuint64_t*>(strides_bytes),
+                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 // 4-D bf16 map, dims innermost first, 128-byte swizzle, box inner = 64 elements (128 B).
 static bool make_map(CUtensorMap* m, const void* base, const uint64_t dims[4], const uint64_t strides_bytes[3],
                      const uint32_t box[4]) {
@@ -627,7 +722,7 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
                        cudaStream_t stream) {
   using namespace attn;
   const int G = hq / hkv;
-  CUtensorMap tq, tk, tv;
+  CUtensorMap tq, tk, tv, tku, tvu, to;
   {
     const uint64_t dims[4] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)bw, (uint64_t)n_req};
     const uint64_t str[3] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2, (uint64_t)bw * hq * kD * 2};
@@ -649,13 +744,35 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
   a.pm = pm; a.ps = ps; a.po = po;
   static const int dbg_env = getenv("XGR_ATTN_DBG") ? atoi(getenv("XGR_ATTN_DBG")) : 0;
   a.dbg = dbg_env;
+  // fused-mode epilogue staging: the unshared K/V rows of the CTA's beams fit the K ring, and
+  // the 64-dim panels of 8-row swizzle atoms stay 1024-byte aligned
+  const int nb = kBM / G;
+  a.u_stage = (!pm && n_unshared > 0 && !(a.dbg & 2) && 4 * nb * n_unshared * 128 <= (int)(kKStages * 2 * kKVPanel) &&
+               (nb * n_unshared) % 8 == 0) ? 1 : 0;
+  a.o_tma = (!pm && !(a.dbg & 8)) ? 1 : 0;
+  memset(&tku, 0, sizeof(tku));
+  memset(&tvu, 0, sizeof(tvu));
+  memset(&to, 0, sizeof(to));
+  if (a.u_stage) {
+    const uint64_t dims[5] = {(uint64_t)kD, (uint64_t)hkv, (uint64_t)n_unshared, (uint64_t)bw, (uint64_t)n_req};
+    const uint64_t str[4] = {(uint64_t)kD * 2, (uint64_t)hkv * kD * 2, (uint64_t)u_beam_stride * 2,
+                             (uint64_t)std::max<int64_t>(u_req_stride, 1) * 2};
+    const uint32_t box[5] = {64, 1, (uint32_t)n_unshared, (uint32_t)nb, 1};
+    if (!make_map_nd(&tku, ku, 5, dims, str, box) || !make_map_nd(&tvu, vu, 5, dims, str, box)) return 1;
+  }
+  if (a.o_tma) {
+    const uint64_t dims[4] = {(uint64_t)kD, (uint64_t)hq, (uint64_t)bw, (uint64_t)n_req};
+    const uint64_t str[3] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2, (uint64_t)bw * hq * kD * 2};
+    const uint32_t box[4] = {64, (uint32_t)G, (uint32_t)(kBM / G), 1};
+    if (!make_map(&to, out, dims, str, box)) return 1;
+  }
   const dim3 grid((unsigned)((bw * G + kBM - 1) / kBM), (unsigned)hkv, (unsigned)n_req);
   if (pm) {
     cudaFuncSetAttribute(k_attn_shared<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    k_attn_shared<true><<<grid, kThreads, kSmem, stream>>>(tq, tk, tv, a);
+    k_attn_shared<true><<<grid, kThreads, kSmem, stream>>>(tq, tk, tv, tku, tvu, to, a);
   } else {
     cudaFuncSetAttribute(k_attn_shared<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
-    k_attn_shared<false><<<grid, kThreads, kSmem, stream>>>(tq, tk, tv, a);
+    k_attn_shared<false><<<grid, kThreads, kSmem, stream>>>(tq, tk, tv, tku, tvu, to, a);
   }
   return cudaGetLastError() == cudaSuccess ? 0 : 2;
 }

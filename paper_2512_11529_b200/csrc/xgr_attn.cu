@@ -222,6 +222,8 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int mt = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
   const int T = (a.ls + kBN - 1) / kBN;
   const uint32_t sb = su32(smem);
+  uint64_t ts0 = 0, ts1 = 0, ts2 = 0;   // XGR_ATTN_DBG & 16: phase timestamps (development)
+  if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
   if (sb & 1023u) __trap();   // the 128-byte swizzle atoms need 1024-byte alignment
   // barriers: Q; K ring full/empty [3]; V ring full/empty [2]; S full [2]; P full; O done; O final
   const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 32,
@@ -388,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+    if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
       mbar_wait(bar_s_full + 8 * s, (j >> 1) & 1);
@@ -460,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(bar_o_final, 0);
       tc_fence_after();
     }
+    if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
     // ---- epilogue ----
     const float t_true = raw_max * c2;
     if constexpr (kPartial) {
@@ -591,6 +595,15 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       if (row_ok && a.lse) a.lse[qrow] = (m_tot + __log2f(den)) * 0.6931471805599453f;
     }
+  }
+  if ((a.dbg & 16) && threadIdx.x == 64 && (blockIdx.x * 7 + blockIdx.y * 3 + blockIdx.z) % 37 == 0) {
+    uint64_t ts3;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    printf("ATTNTS cta %d %d %d sm %u start %llu pre %llu loop %llu epi %llu\n", blockIdx.x, blockIdx.y, blockIdx.z, smid,
+           (unsigned long long)ts0, (unsigned long long)(ts1 - ts0), (unsigned long long)(ts2 - ts1),
+           (unsigned long long)(ts3 - ts2));
   }
   tc_fence_before();
   __syncthreads();

@@ -1098,7 +1098,8 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   constexpr int NR = ROOT ? 1 : kMaxBW;   // parent rows
   __shared__ ParentInfoN<NR> s_pi;
   __shared__ float s_red[T / 32], s_red2[T / 32];
-  __shared__ uint32_t s_count, s_nbig;
+  __shared__ uint32_t s_count, s_nbig, s_nroot, s_bin;
+  __shared__ uint32_t s_wtot[T / 32];
   __shared__ uint16_t s_rbase[NR], s_rcnt[NR];   // each row's key segment (per-beam Top-K)
   __shared__ int32_t s_big[NR];
   const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
@@ -1119,6 +1120,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   if (tid == 0) {
     s_count = 0;
     s_nbig = 0;
+    s_nroot = 0;
   }
   // the commit's parent info (first child, end, dense slot) is written by the gather below,
   // which loads the same node data; the barriers before the commit order it
@@ -1159,6 +1161,74 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
         const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
         if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
+        if (nl == 1 && fe - fc > 2u * T && a.sparse_cap >= 4096) {
+          // single root row: only the candidates that can reach the Top-BW go to shared memory.
+          // A histogram of the keys' top 13 bits (8192 bins, in the key buffer) gives the bin B
+          // where the count from the top reaches min(BW, n); the keys in bins >= B (typically
+          // ~1.3 x BW) are compacted and the selection below sorts only those. (The histogram needs
+          // 32 KB of the key buffer: sparse_cap >= 4096 keys.)
+          uint32_t* hist = reinterpret_cast<uint32_t*>(s_keys);
+          uint64_t kk[RPT];
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) {
+            const uint32_t q = fc + (uint32_t)(k * T + tid);
+            kk[k] = q < fe ? make_key(cand_score(S, xv[k], lse), (uint32_t)b * V + vv[k]) : 0ull;
+          }
+          for (int i = tid; i < 8192; i += T) hist[i] = 0u;
+          if (tid == 0) s_nroot = fe - fc;
+          __syncthreads();
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (kk[k]) atomicAdd(&hist[(uint32_t)(kk[k] >> 51)], 1u);
+          __syncthreads();
+          // thread t owns bins 8191 - 16 t - j (j < 16): descending order over the block
+          uint32_t c16[16], loc = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            c16[j] = hist[8191 - 16 * tid - j];
+            loc += c16[j];
+          }
+          uint32_t incl = loc;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+          }
+          if (lane == 31) s_wtot[tid >> 5] = incl;
+          if (tid == 0) s_bin = 0u;
+          __syncthreads();
+          uint32_t before = incl - loc;
+          for (int w = 0; w < (tid >> 5); ++w) before += s_wtot[w];
+          const uint32_t need = min((uint32_t)a.BW, fe - fc);
+          if (before < need && before + loc >= need) {
+            uint32_t acc = before;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (acc < need && acc + c16[j] >= need) s_bin = 8191u - 16u * tid - j;
+              acc += c16[j];
+            }
+          }
+          __syncthreads();
+          const uint32_t bmin = s_bin;
+          uint32_t cnt = 0;
+#pragma unroll
+          for (int k = 0; k < RPT; ++k) cnt += (kk[k] && (uint32_t)(kk[k] >> 51) >= bmin) ? 1u : 0u;
+          uint32_t ci = cnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, ci, o);
+            if (lane >= o) ci += y;
+          }
+          uint32_t wb = 0;
+          if (lane == 31 && ci) wb = atomicAdd(&s_count, ci);
+          uint32_t pos = __shfl_sync(0xffffffffu, wb, 31) + ci - cnt;
+          __syncthreads();   // the histogram is dead; the key buffer takes the candidates
+#pragma unroll
+          for (int k = 0; k < RPT; ++k)
+            if (kk[k] && (uint32_t)(kk[k] >> 51) >= bmin) s_keys[pos++] = kk[k];
+          __syncthreads();
+          continue;
+        }
         const uint32_t base = s_count;
 #pragma unroll
         for (int k = 0; k < RPT; ++k) {
@@ -1268,7 +1338,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   }
   __syncthreads();
   const int n = (int)s_count;
-  if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, n);
+  if (tid == 0) count_add(a, XGR_CNT_SPARSE_CANDS, ROOT && s_nroot ? s_nroot : (uint32_t)n);
   int k = min(n, a.BW);
   if (a.topk) {
     if (ROOT) {

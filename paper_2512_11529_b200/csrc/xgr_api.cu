@@ -75,7 +75,9 @@ static constexpr int kTimingRing = 4096;
 
 namespace xgr {
 bool pdl_enabled() {
-  static const bool on = !(getenv("XGR_PDL") && atoi(getenv("XGR_PDL")) == 0);
+  // off by default: neutral in eager streams (0.477 vs 0.475 ms per C3 pass) and slower inside
+  // CUDA graphs (0.644 vs 0.438 ms); XGR_PDL=1 enables it
+  static const bool on = getenv("XGR_PDL") && atoi(getenv("XGR_PDL")) == 1;
   return on;
 }
 }  // namespace xgr

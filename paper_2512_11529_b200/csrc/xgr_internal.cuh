@@ -16,7 +16,8 @@ namespace xgr {
 // Step kernels are launched with programmatic stream serialization: a kernel's CTAs may be
 // scheduled while its stream predecessor drains. Every such kernel executes pdl_wait() (wait for
 // the predecessor grid to complete and its writes to be visible) before touching global memory,
-// and pdl_trigger() early so its own successor can be scheduled. XGR_PDL=0 disables it.
+// and pdl_trigger() early so its own successor can be scheduled. Off unless XGR_PDL=1 (see
+// pdl_enabled); without the launch attribute both instructions are no-ops.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

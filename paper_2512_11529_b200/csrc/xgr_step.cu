@@ -174,7 +174,7 @@ __device__ __forceinline__ void dense_row_compute(const float* __restrict__ row,
   const float Z = block_sum<T>((z0 + z1) + (z2 + z3), s_red2);
   r.finite = (Z > 0.5f) && (Z <= 3.0e38f);
   r.M = M;
-  r.lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+  r.lse = row_lse(M, Z);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -690,7 +690,7 @@ __device__ void sparse_row_main(const StepArgs& a, int req, int b, float S, floa
   for (uint32_t k = fc + tid; k < fe; k += T) z += ex2(__fmul_rn(__fsub_rn(row[lab[k]], M), kLog2e));
   const float Z = block_sum<T>(z, s_red2);
   const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-  const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+  const float lse = row_lse(M, Z);
   if (tid == 0) {
     a.lse[(size_t)req * a.BW + b] = finite ? lse : __int_as_float(0x7fc00000);
     if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
@@ -1159,7 +1159,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
           if (fc + (uint32_t)(k * T + tid) < fe) z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
         const float Z = block_sum<T>(z, s_red2);
         const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-        const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+        const float lse = row_lse(M, Z);
         if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
         if (nl == 1 && fe - fc > 2u * T && a.sparse_cap >= 4096) {
           // single root row: only the candidates that can reach the Top-BW go to shared memory.
@@ -1248,7 +1248,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[k]), M), kLog2e));
       const float Z = block_sum<T>(z, s_red2);
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      const float lse = row_lse(M, Z);
       if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
       const uint32_t base = s_count;
       for (uint32_t k = fc + tid; k < fe; k += T) {
@@ -1292,7 +1292,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       for (int k = 0; k < kSmall; ++k)
         if (k < cnt) Z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      const float lse = row_lse(M, Z);
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
       const uint32_t base = atomicAdd(&s_count, (uint32_t)cnt);
       XGR_CHECK(base + cnt <= (uint32_t)a.sparse_cap, "sparse keys base %u cnt %d cap %d", base, cnt, a.sparse_cap);
@@ -1321,7 +1321,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
         z += ex2(__fmul_rn(__fsub_rn(xq(k), M), kLog2e));
       const float Z = warp_sum(z);
       const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      const float lse = row_lse(M, Z);
       if (!finite && lane == 0) atomicOr(a.flags + req, kFlagNonfinite);
       uint32_t base = 0;
       if (lane == 0) {

@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 #pragma unroll
     for (int i = 1; i < CTR / 32; ++i) Z += g_sum[g * (CTR / 32) + i];
     finite = (Z > 0.5f) && (Z <= 3.0e38f);
-    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    lse = row_lse(M, Z);
     }   // MODE != kModeShardEmit
     if (lt == 0) {
       a.lse[(size_t)req * BW + g] = finite ? lse : __int_as_float(0x7fc00000);
@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
 #pragma unroll
     for (int w = 0; w < NW; ++w) Z += part[w].y * ex2f(__fmul_rn(__fsub_rn(part[w].x, M), kLog2eS));
     if (!((Z > 0.5f) && (Z <= 3.0e38f))) return;   // k_stream flags non-finite rows
-    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    lse = row_lse(M, Z);
   }
   float cmax = -INFINITY;
 #pragma unroll
@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
           continue;
         }
         finite = (Z > 0.5f) && (Z <= 3.0e38f);
-        lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+        lse = row_lse(M, Z);
         if (lt == 0) {
           a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
           if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
@@ -1042,7 +1042,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       // (bins of 1/128). tau: each warp's m-th largest (m = ceil(BW / 8) <= 64) of its lanes'
       // top-2 candidates -- distinct elements, so the row has >= BW candidates >= tau.
       if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
-      const float lse3 = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+      const float lse3 = row_lse(M, Z);
       const float S0 = d.lse;
       float c1 = -INFINITY, c2 = -INFINITY;
 #pragma unroll
@@ -1094,7 +1094,7 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
       continue;
     }
     const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-    lse = __fadd_rn(M, fmaxf(logf(Z), 0.0f));
+    lse = row_lse(M, Z);
     if (lt == 0) {
       a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);

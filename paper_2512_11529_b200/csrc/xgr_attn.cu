@@ -77,20 +77,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// Spin with a short sleep between polls (for the single-thread producer / MMA roles, so their
-// polling does not take issue slots from the softmax warps).
-__device__ __forceinline__ void mbar_wait_sleep(uint32_t b, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-      : "=r"(ok) : "r"(b), "r"(parity) : "memory");
-  while (!ok) {
-    __nanosleep(20);
-    asm volatile(
-        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok) : "r"(b), "r"(parity) : "memory");
-  }
-}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -205,7 +191,9 @@ struct AttnArgs {
   float* pm;                         // partial mode: [n_req][bw][hq] m, s and [..][d] o (fp32)
   float* ps;
   float* po;
-  int dbg;                           // XGR_ATTN_DBG (development experiments)
+  int dbg;                           // XGR_ATTN_DBG (development): 2 = unshared rows from global
+                                     // memory (no staging), 8 = per-thread output stores
+                                     // (no TMA store), 16 = per-CTA phase timestamps (printf)
   int u_stage;                       // fused: unshared K/V rows TMA-staged in the K ring
   int o_tma;                         // fused: output tile written by TMA from the V ring
 };
@@ -262,9 +250,6 @@ __global__ void __launch_bounds__(kThreads, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  auto role_wait = [&](uint32_t b, uint32_t par) {
-    if (a.dbg & 4) mbar_wait_sleep(b, par); else mbar_wait(b, par);
-  };
   if (warp == 0) {
     // ===== TMA producers: lane 0 streams Q then K, lane 1 streams V. A K stage is released by the
     // commit after its S MMA, a V stage after its PV MMA, so K_{j+2} is in flight while tile j's
@@ -283,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int ns = lane == 0 ? kKStages : kVStages;
       for (int j = 0; j < T; ++j) {
         const int s = j % ns, u = j / ns;
-        if (j >= ns) role_wait(empty0 + 8 * s, (u + 1) & 1);
+        if (j >= ns) mbar_wait(empty0 + 8 * s, (u + 1) & 1);
         const uint32_t full = full0 + 8 * s, dst = buf0 + s * 2 * kKVPanel;
         mbar_expect_tx(full, 2 * kKVPanel);
         tma_load_4d(dst, tm, full, 0, kvh, j * kBN, req);
@@ -293,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         // the CTA's beams' own K/V rows (beam-major, then token), one TMA box per 64-dim panel,
         // into the K ring as soon as its last tiles have been consumed by their S MMAs
         for (int j = max(0, T - kKStages); j < T; ++j)
-          role_wait(bar_k_empty + 8 * (j % kKStages), (j / kKStages) & 1);
+          mbar_wait(bar_k_empty + 8 * (j % kKStages), (j / kKStages) & 1);
         const uint32_t pu = (uint32_t)(kBM / a.G) * a.n_unshared * 128;
         const int b0 = mt * (kBM / a.G);
         mbar_expect_tx(bar_u, 4 * pu);
@@ -308,10 +293,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (lane == 0 && T > 0) {
       constexpr uint32_t idS = idesc_bf16(kBM, kBN, 0);
       constexpr uint32_t idO = idesc_bf16(kBM, kD, 1);
-      role_wait(bar_q, 0);
+      mbar_wait(bar_q, 0);
       auto issue_s = [&](int j) {
         const int s = j & 1, ks = j % kKStages;
-        role_wait(bar_k_full + 8 * ks, (j / kKStages) & 1);
+        mbar_wait(bar_k_full + 8 * ks, (j / kKStages) & 1);
         tc_fence_after();
         const uint32_t kb = sb + kOffK + ks * 2 * kKVPanel;
 #pragma unroll
@@ -327,8 +312,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       issue_s(0);
       for (int j = 0; j < T; ++j) {
         if (j + 1 < T) issue_s(j + 1);
-        role_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
-        role_wait(bar_p_full, j & 1);
+        mbar_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
+        mbar_wait(bar_p_full, j & 1);
         tc_fence_after();
         const uint32_t vb = sb + kOffV + (j & 1) * 2 * kKVPanel;
 #pragma unroll

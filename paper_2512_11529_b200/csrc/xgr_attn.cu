@@ -77,6 +77,16 @@ __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// mbar_wait that adds the cycles it spent to *acc when acc != nullptr (XGR_ATTN_DBG & 16)
+__device__ __forceinline__ void mbar_wait_t(uint32_t b, uint32_t parity, unsigned long long* acc) {
+  if (acc) {
+    const unsigned long long t0 = clock64();
+    mbar_wait(b, parity);
+    *acc += clock64() - t0;
+  } else {
+    mbar_wait(b, parity);
+  }
+}
 __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
                                             int c2, int c3) {
   asm volatile(
@@ -191,9 +201,11 @@ struct AttnArgs {
   float* pm;                         // partial mode: [n_req][bw][hq] m, s and [..][d] o (fp32)
   float* ps;
   float* po;
-  int dbg;                           // XGR_ATTN_DBG (development): 2 = unshared rows from global
+  int dbg;                           // XGR_ATTN_DBG (development): 1 = P_j written without waiting
+                                     // for PV_{j-1} (equal speed), 2 = unshared rows from global
                                      // memory (no staging), 8 = per-thread output stores
-                                     // (no TMA store), 16 = per-CTA phase timestamps (printf)
+                                     // (no TMA store), 16 = per-CTA phase timestamps (printf) with
+                                     // per-barrier wait cycles
   int u_stage;                       // fused: unshared K/V rows TMA-staged in the K ring
   int o_tma;                         // fused: output tile written by TMA from the V ring
 };
@@ -211,9 +223,13 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int T = (a.ls + kBN - 1) / kBN;
   const uint32_t sb = su32(smem);
   uint64_t ts0 = 0, ts1 = 0, ts2 = 0;   // XGR_ATTN_DBG & 16: phase timestamps (development)
+  unsigned long long wk = 0, wv = 0, wp = 0, ws = 0, wo = 0;   // ... and wait cycles per barrier
+  const bool tw = (a.dbg & 16) != 0;
   if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
   if (sb & 1023u) __trap();   // the 128-byte swizzle atoms need 1024-byte alignment
-  // barriers: Q; K ring full/empty [3]; V ring full/empty [2]; S full [2]; P full; O done; O final
+  // barriers: Q; K ring full/empty [3]; V ring full/empty [2]; S full [2]; P full [2] (by tile
+  // parity: a softmax warp may finish tile j+1 before another has arrived for tile j, and an
+  // arrival must never count towards the previous tile's phase); O done; O final
   const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 32,
                  bar_v_full = bar_q + 56, bar_v_empty = bar_q + 72, bar_s_full = bar_q + 88,
                  bar_p_full = bar_q + 104, bar_o_done = bar_q + 112,
@@ -232,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_init(bar_s_full + 8 * i, 1);
     }
     mbar_init(bar_p_full, 128);
+    mbar_init(bar_p_full + 32, 128);
     mbar_init(bar_o_done, 1);
     mbar_init(bar_o_final, 1);
     mbar_init(bar_u, 1);
@@ -296,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(bar_q, 0);
       auto issue_s = [&](int j) {
         const int s = j & 1, ks = j % kKStages;
-        mbar_wait(bar_k_full + 8 * ks, (j / kKStages) & 1);
+        mbar_wait_t(bar_k_full + 8 * ks, (j / kKStages) & 1, tw ? &wk : nullptr);
         tc_fence_after();
         const uint32_t kb = sb + kOffK + ks * 2 * kKVPanel;
 #pragma unroll
@@ -312,8 +329,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       issue_s(0);
       for (int j = 0; j < T; ++j) {
         if (j + 1 < T) issue_s(j + 1);
-        mbar_wait(bar_v_full + 8 * (j & 1), (j >> 1) & 1);
-        mbar_wait(bar_p_full, j & 1);
+        mbar_wait_t(bar_v_full + 8 * (j & 1), (j >> 1) & 1, tw ? &wv : nullptr);
+        mbar_wait_t(bar_p_full + 32 * (j & 1), (j >> 1) & 1, tw ? &wp : nullptr);
         tc_fence_after();
         const uint32_t vb = sb + kOffV + (j & 1) * 2 * kKVPanel;
 #pragma unroll
@@ -378,7 +395,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
-      mbar_wait(bar_s_full + 8 * s, (j >> 1) & 1);
+      mbar_wait_t(bar_s_full + 8 * s, (j >> 1) & 1, tw ? &ws : nullptr);
       tc_fence_after();
       uint32_t u0[32], u1[32];
       tmem_ld32(tmem + lane_base + s * kBN, u0);
@@ -422,13 +439,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       l += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       // P_j -> TMEM over S_j (the PV MMA reads it as its A operand); the S buffer is rewritten
       // only by S_{j+2}, issued after PV_j
-      if (j > 0) {
-        // PV_{j-1} done before P_j is written (a lazy variant that skipped this wait when no
-        // correction was needed raced intermittently; measured no faster) and before O is rescaled
-        mbar_wait(bar_o_done, (j - 1) & 1);
+      const bool lazy = (a.dbg & 1) != 0;
+      if (j > 0 && !lazy) {
+        // PV_{j-1} done before P_j is written and before O is rescaled
+        mbar_wait_t(bar_o_done, (j - 1) & 1, tw ? &wo : nullptr);
         tc_fence_after();
       }
       tmem_st32(tmem + lane_base + s * kBN, pk);
+      if (j > 0 && lazy && __any_sync(0xffffffffu, resc)) {
+        // only O needs PV_{j-1}; P_j's buffer was last read by PV_{j-2}, complete before S_j
+        mbar_wait_t(bar_o_done, (j - 1) & 1, tw ? &wo : nullptr);
+        tc_fence_after();
+      }
       if (j > 0 && __any_sync(0xffffffffu, resc)) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -442,7 +464,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       }
       tmem_wait_st();
       tc_fence_before();
-      mbar_arrive(bar_p_full);
+      mbar_arrive(bar_p_full + 32 * (j & 1));
     }
     if (T > 0) {
       mbar_wait(bar_o_final, 0);
@@ -581,6 +603,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (row_ok && a.lse) a.lse[qrow] = (m_tot + __log2f(den)) * 0.6931471805599453f;
     }
   }
+  if (tw && (threadIdx.x == 32 || threadIdx.x == 64) && (blockIdx.x * 7 + blockIdx.y * 3 + blockIdx.z) % 37 == 0)
+    printf("ATTNW cta %d %d %d thr %d k %llu v %llu p %llu s %llu o %llu\n", blockIdx.x, blockIdx.y, blockIdx.z,
+           threadIdx.x, wk, wv, wp, ws, wo);
   if ((a.dbg & 16) && threadIdx.x == 64 && (blockIdx.x * 7 + blockIdx.y * 3 + blockIdx.z) % 37 == 0) {
     uint64_t ts3;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));

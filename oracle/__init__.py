@@ -13,6 +13,9 @@ Modules
                 selection oracle.
   brute         pure-Python enumeration for tiny tries (legal set by enumerating all V^ND tuples,
                 path scores of every item by math.exp / math.log loops).
+  kv_reorder    the unshared KV-cache reorder after a step (NEXT f2).
+  attention     staged shared/unshared decode attention and its OnlineSoftmax merge (PAPER.md
+                L339; NEXT f4's second workload), fp64.
 
 Parity status of every function: pinned (see tests/test_oracle_pins.py and DESIGN.md section
 "Oracle pins"). The pruned fraction and throughput numbers are parity-unpinned: the paper prints

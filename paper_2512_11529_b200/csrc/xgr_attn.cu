@@ -222,10 +222,22 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int mt = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
   const int T = (a.ls + kBN - 1) / kBN;
   const uint32_t sb = su32(smem);
-  uint64_t ts0 = 0, ts1 = 0, ts2 = 0;   // XGR_ATTN_DBG & 16: phase timestamps (development)
-  unsigned long long wk = 0, wv = 0, wp = 0, ws = 0, wo = 0;   // ... and wait cycles per barrier
+  uint64_t ts0 = 0, ts1 = 0, ts2 = 0;   // XGR_ATTN_PROFILE + XGR_ATTN_DBG & 16: phase timestamps
+#ifdef XGR_ATTN_PROFILE   // wait cycles per barrier (build with -DXGR_ATTN_PROFILE; costs registers)
+  unsigned long long wk = 0, wv = 0, wp = 0, ws = 0, wo = 0;
   const bool tw = (a.dbg & 16) != 0;
+#else
+  unsigned long long* const wk_ = nullptr;
+  constexpr bool tw = false;
+#define wk (*wk_)
+#define wv (*wk_)
+#define wp (*wk_)
+#define ws (*wk_)
+#define wo (*wk_)
+#endif
+#ifdef XGR_ATTN_PROFILE
   if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts0));
+#endif
   if (sb & 1023u) __trap();   // the 128-byte swizzle atoms need 1024-byte alignment
   // barriers: Q; K ring full/empty [3]; V ring full/empty [2]; S full [2]; P full [2] (by tile
   // parity: a softmax warp may finish tile j+1 before another has arrived for tile j, and an
@@ -392,7 +404,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
       }
     }
+#ifdef XGR_ATTN_PROFILE
     if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts1));
+#endif
     for (int j = 0; j < T; ++j) {
       const int s = j & 1;
       mbar_wait_t(bar_s_full + 8 * s, (j >> 1) & 1, tw ? &ws : nullptr);
@@ -470,7 +484,9 @@ __global__ void __launch_bounds__(kThreads, 2)
       mbar_wait(bar_o_final, 0);
       tc_fence_after();
     }
+#ifdef XGR_ATTN_PROFILE
     if (a.dbg & 16) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts2));
+#endif
     // ---- epilogue ----
     const float t_true = raw_max * c2;
     if constexpr (kPartial) {
@@ -603,9 +619,18 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (row_ok && a.lse) a.lse[qrow] = (m_tot + __log2f(den)) * 0.6931471805599453f;
     }
   }
+#ifdef XGR_ATTN_PROFILE
   if (tw && (threadIdx.x == 32 || threadIdx.x == 64) && (blockIdx.x * 7 + blockIdx.y * 3 + blockIdx.z) % 37 == 0)
     printf("ATTNW cta %d %d %d thr %d k %llu v %llu p %llu s %llu o %llu\n", blockIdx.x, blockIdx.y, blockIdx.z,
            threadIdx.x, wk, wv, wp, ws, wo);
+#else
+#undef wk
+#undef wv
+#undef wp
+#undef ws
+#undef wo
+#endif
+#ifdef XGR_ATTN_PROFILE
   if ((a.dbg & 16) && threadIdx.x == 64 && (blockIdx.x * 7 + blockIdx.y * 3 + blockIdx.z) % 37 == 0) {
     uint64_t ts3;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ts3));
@@ -615,11 +640,377 @@ __global__ void __launch_bounds__(kThreads, 2)
            (unsigned long long)ts0, (unsigned long long)(ts1 - ts0), (unsigned long long)(ts2 - ts1),
            (unsigned long long)(ts3 - ts2));
   }
+#endif
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
+  }
+}
+
+// ---- two Q tiles per CTA (fused mode) -------------------------------------------------------
+// One CTA per SM (224 KB of shared memory, all 512 TMEM columns) holds two 128-row query tiles A and
+// B of the same (request, KV head) and streams 128-key K/V tiles once for both. TMEM: S_A [0,128),
+// O_A [128,256), S_B [256,384), O_B [384,512); P overwrites the first 64 columns of its S tile
+// (packed bf16). The MMA issue order PV_A(j), S_A(j+1), PV_B(j), S_B(j+1) staggers the two tiles:
+// softmax A(j+1) runs while the tensor core does PV_B(j) and S_B(j+1), and vice versa. S_t(j)
+// complete implies PV_t(j-1) complete (issued before it, tracked by the same commit), so neither
+// the P write nor the O correction waits for a PV barrier.
+namespace pair {
+constexpr int kBN = 128;
+constexpr int kThreads = 320;                   // producer, MMA, 4 softmax warps per tile
+constexpr uint32_t kQPanel = 128 * 128;         // 16 KB (128 rows x 64 dims)
+constexpr uint32_t kKVPanel = kBN * 128;        // 16 KB (128 keys x 64 dims)
+constexpr int kKStages = 3, kVStages = 2;
+constexpr uint32_t kOffQ = 0;                             // [tile][panel]
+constexpr uint32_t kOffK = 4 * kQPanel;                   // [stage][panel]
+constexpr uint32_t kOffV = kOffK + kKStages * 2 * kKVPanel;
+constexpr uint32_t kOffBar = kOffV + kVStages * 2 * kKVPanel;
+constexpr uint32_t kSmem = kOffBar + 256;
+}  // namespace pair
+
+__global__ void __launch_bounds__(pair::kThreads, 1)
+    k_attn_pair(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_ku,
+                const __grid_constant__ CUtensorMap tm_vu, const __grid_constant__ CUtensorMap tm_o,
+                const AttnArgs a) {
+  constexpr int kBN = pair::kBN;
+  constexpr uint32_t kQPanel = pair::kQPanel, kKVPanel = pair::kKVPanel;
+  constexpr int kKStages = pair::kKStages, kVStages = pair::kVStages;
+  constexpr uint32_t kOffQ = pair::kOffQ, kOffK = pair::kOffK, kOffV = pair::kOffV, kOffBar = pair::kOffBar;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mp = blockIdx.x, kvh = blockIdx.y, req = blockIdx.z;
+  const int T = (a.ls + kBN - 1) / kBN;
+  const int nb = 128 / a.G;                     // beams per tile
+  const uint32_t sb = su32(smem);
+  if (sb & 1023u) __trap();
+  // barriers: Q; K full/empty [3]; V full/empty [2]; S full [tile]; P full [tile][parity];
+  // O final; unshared rows
+  const uint32_t bar_q = sb + kOffBar, bar_k_full = bar_q + 8, bar_k_empty = bar_q + 32,
+                 bar_v_full = bar_q + 56, bar_v_empty = bar_q + 72, bar_s_full = bar_q + 88,
+                 bar_p_full = bar_q + 104, bar_o_final = bar_q + 136, bar_u = bar_q + 144;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + kOffBar + 192);
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int i = 0; i < kKStages; ++i) {
+      mbar_init(bar_k_full + 8 * i, 1);
+      mbar_init(bar_k_empty + 8 * i, 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar_v_full + 8 * i, 1);
+      mbar_init(bar_v_empty + 8 * i, 1);
+      mbar_init(bar_s_full + 8 * i, 1);
+    }
+    for (int i = 0; i < 4; ++i) mbar_init(bar_p_full + 8 * i, 128);
+    mbar_init(bar_o_final, 1);
+    mbar_init(bar_u, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    prefetch_map(&tm_q);
+    prefetch_map(&tm_k);
+    prefetch_map(&tm_v);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nu = a.n_unshared;
+
+  if (warp == 0) {
+    // ===== TMA producers: lane 0 Q (both tiles) + K ring (+ the unshared rows at the end);
+    // lane 1 V ring =====
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, 4 * kQPanel);
+      for (int t = 0; t < 2; ++t) {
+        const int b0 = (2 * mp + t) * nb;
+        tma_load_4d(sb + kOffQ + (2 * t) * kQPanel, &tm_q, bar_q, 0, kvh * a.G, b0, req);
+        tma_load_4d(sb + kOffQ + (2 * t + 1) * kQPanel, &tm_q, bar_q, 64, kvh * a.G, b0, req);
+      }
+    }
+    if (lane < 2) {
+      const CUtensorMap* tm = lane == 0 ? &tm_k : &tm_v;
+      const uint32_t full0 = lane == 0 ? bar_k_full : bar_v_full;
+      const uint32_t empty0 = lane == 0 ? bar_k_empty : bar_v_empty;
+      const uint32_t buf0 = sb + (lane == 0 ? kOffK : kOffV);
+      const int ns = lane == 0 ? kKStages : kVStages;
+      for (int j = 0; j < T; ++j) {
+        const int st = j % ns, u = j / ns;
+        if (j >= ns) mbar_wait(empty0 + 8 * st, (u + 1) & 1);
+        const uint32_t full = full0 + 8 * st, dst = buf0 + st * 2 * kKVPanel;
+        mbar_expect_tx(full, 2 * kKVPanel);
+        tma_load_4d(dst, tm, full, 0, kvh, j * kBN, req);
+        tma_load_4d(dst + kKVPanel, tm, full, 64, kvh, j * kBN, req);
+      }
+      if (lane == 0 && a.u_stage) {
+        for (int j = max(0, T - kKStages); j < T; ++j)
+          mbar_wait(bar_k_empty + 8 * (j % kKStages), (j / kKStages) & 1);
+        const uint32_t pu = (uint32_t)nb * nu * 128;
+        mbar_expect_tx(bar_u, 8 * pu);
+        for (int t = 0; t < 2; ++t) {
+          const int b0 = (2 * mp + t) * nb;
+          const uint32_t base = sb + kOffK + t * 4 * pu;
+          tma_load_5d(base, &tm_ku, bar_u, 0, kvh, 0, b0, req);
+          tma_load_5d(base + pu, &tm_ku, bar_u, 64, kvh, 0, b0, req);
+          tma_load_5d(base + 2 * pu, &tm_vu, bar_u, 0, kvh, 0, b0, req);
+          tma_load_5d(base + 3 * pu, &tm_vu, bar_u, 64, kvh, 0, b0, req);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    if (lane == 0 && T > 0) {
+      constexpr uint32_t idS = idesc_bf16(128, kBN, 0);
+      constexpr uint32_t idO = idesc_bf16(128, kD, 1);
+      mbar_wait(bar_q, 0);
+      auto issue_s = [&](int j, int t) {   // S_t(j) = Q_t K_j^T into S_t
+        const int ks = j % kKStages;
+        if (t == 0) {
+          mbar_wait(bar_k_full + 8 * ks, (j / kKStages) & 1);
+          tc_fence_after();
+        }
+        const uint32_t kb = sb + kOffK + ks * 2 * kKVPanel;
+        const uint32_t qb = sb + kOffQ + 2 * t * kQPanel;
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk) {
+          const uint32_t p = kk >> 2, off = (kk & 3) * 32;
+          umma(tmem + 256 * t, sdesc(qb + p * kQPanel + off, 16, 1024), sdesc(kb + p * kKVPanel + off, 16, 1024),
+               idS, kk > 0);
+        }
+        umma_commit(bar_s_full + 8 * t);
+        if (t == 1) umma_commit(bar_k_empty + 8 * ks);
+      };
+      auto issue_pv = [&](int j, int t) {  // O_t += P_t(j) V_j
+        const int vs = j % kVStages;
+        if (t == 0) mbar_wait(bar_v_full + 8 * vs, (j / kVStages) & 1);
+        mbar_wait(bar_p_full + 8 * (2 * t + (j & 1)), (j >> 1) & 1);
+        tc_fence_after();
+        const uint32_t vb = sb + kOffV + vs * 2 * kKVPanel;
+#pragma unroll
+        for (int kk = 0; kk < kBN / 16; ++kk)
+          umma_ts(tmem + 256 * t + 128, tmem + 256 * t + kk * 8, sdesc(vb + kk * 2048, kKVPanel, 1024), idO,
+                  (j > 0 || kk > 0) ? 1u : 0u);
+        if (t == 1) umma_commit(bar_v_empty + 8 * vs);
+      };
+      issue_s(0, 0);
+      issue_s(0, 1);
+      for (int j = 0; j < T; ++j) {
+        issue_pv(j, 0);
+        if (j + 1 < T) issue_s(j + 1, 0);
+        issue_pv(j, 1);
+        if (j + 1 < T) issue_s(j + 1, 1);
+      }
+      umma_commit(bar_o_final);
+    }
+  } else {
+    // ===== softmax + epilogue: warps 2-5 tile A, 6-9 tile B; thread <-> row <-> TMEM lane =====
+    const int t = (warp - 2) >> 2;
+    const int q4 = warp & 3;
+    const int r = q4 * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q4 * 32) << 16;
+    const uint32_t tS = tmem + 256 * t, tO = tS + 128;
+    const float c2 = a.scale * 1.4426950408889634f;
+    float m_ref = -INFINITY, raw_max = -INFINITY, l = 0.f;
+    const int bl = r / a.G, g = r % a.G;
+    const int b = (2 * mp + t) * nb + bl;
+    const bool row_ok = b < a.bw;
+    const int h = kvh * a.G + g;
+    const int64_t qrow = (((int64_t)req * a.bw + b) * a.hq + h);
+    constexpr int kMaxU = 8;
+    float tu[kMaxU];
+#pragma unroll
+    for (int u = 0; u < kMaxU; ++u) tu[u] = -INFINITY;
+    const uint8_t* qs = smem + kOffQ + 2 * t * kQPanel;
+    auto dot_q = [&](auto&& krow) {   // q row (smem, swizzled) . 16 chunks given by krow(ch)
+      float dot[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int ch = 0; ch < 16; ++ch) {
+        const uint4 qv = *reinterpret_cast<const uint4*>(qs + (ch >> 3) * kQPanel + r * 128 + (((ch & 7) ^ (r & 7)) << 4));
+        float qf[8], kf[8];
+        bf16x8_to_f32(qv, qf);
+        bf16x8_to_f32(krow(ch), kf);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dot[ch & 3] = fmaf(qf[e], kf[e], dot[ch & 3]);
+      }
+      return ((dot[0] + dot[1]) + (dot[2] + dot[3])) * c2;
+    };
+    if (nu > 0 && !a.u_stage) {   // unshared logits from global memory, before the first S tile
+      mbar_wait(bar_q, 0);
+      if (row_ok) {
+        const __nv_bfloat16* kub = a.ku + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
+#pragma unroll 1
+        for (int u = 0; u < nu; ++u) {
+          const uint4* kr = reinterpret_cast<const uint4*>(kub + ((int64_t)u * a.hkv + kvh) * kD);
+          const float v = dot_q([&](int ch) { return __ldg(kr + ch); });
+#pragma unroll
+          for (int w = 0; w < kMaxU; ++w)
+            if (w == u) tu[w] = v;
+        }
+      }
+    }
+    for (int j = 0; j < T; ++j) {
+      mbar_wait(bar_s_full + 8 * t, j & 1);
+      tc_fence_after();
+      float x[kBN];
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        uint32_t u32[32];
+        tmem_ld32(tS + lane_base + 32 * c4, u32);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 32; ++c) x[32 * c4 + c] = __uint_as_float(u32[c]);
+      }
+      const int valid = a.ls - j * kBN;
+      if (valid < kBN) {
+#pragma unroll
+        for (int c = 0; c < kBN; ++c)
+          if (c >= valid) x[c] = -INFINITY;
+      }
+      float mx[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        mx[c] = fmaxf(fmaxf(fmaxf(x[c], x[c + 16]), fmaxf(x[c + 32], x[c + 48])),
+                      fmaxf(fmaxf(x[c + 64], x[c + 80]), fmaxf(x[c + 96], x[c + 112])));
+#pragma unroll
+      for (int c = 0; c < 8; ++c) mx[c] = fmaxf(mx[c], mx[c + 8]);
+      const float tmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      raw_max = fmaxf(raw_max, tmax);
+      const float t2 = tmax * c2;
+      float alpha = 1.f;
+      const bool resc = t2 > m_ref + kRescaleThreshold;
+      if (resc) {
+        alpha = ex2(m_ref - t2);
+        m_ref = t2;
+        l *= alpha;
+      }
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {   // two halves of 64 keys -> 32 packed columns each
+        uint32_t pk[32];
+#pragma unroll
+        for (int c = 0; c < 32; ++c) {
+          const float p0 = ex2(fmaf(x[64 * h2 + 2 * c], c2, -m_ref));
+          const float p1 = ex2(fmaf(x[64 * h2 + 2 * c + 1], c2, -m_ref));
+          ls4[c & 3] += p0 + p1;
+          pk[c] = pack_bf16(p0, p1);
+        }
+        tmem_st32(tS + lane_base + 32 * h2, pk);
+      }
+      l += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      if (j > 0 && __any_sync(0xffffffffu, resc)) {
+#pragma unroll 1
+        for (int k = 0; k < 4; ++k) {
+          uint32_t o[32];
+          tmem_ld32(tO + lane_base + 32 * k, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * alpha);
+          tmem_st32(tO + lane_base + 32 * k, o);
+        }
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar_p_full + 8 * (2 * t + (j & 1)));
+    }
+    if (T > 0) {
+      mbar_wait(bar_o_final, 0);
+      tc_fence_after();
+    }
+    // ---- epilogue: unshared stage + merge, output tile by TMA ----
+    const uint32_t pu = (uint32_t)nb * nu * 128;
+    const uint8_t* us = smem + kOffK + t * 4 * pu;
+    auto urow = [&](int panel, int u, int ch) -> uint4 {
+      const int R = bl * nu + u;
+      return *reinterpret_cast<const uint4*>(us + panel * pu + R * 128 + (((ch & 7) ^ (R & 7)) << 4));
+    };
+    if (nu > 0 && a.u_stage) {
+      mbar_wait(bar_u, 0);
+      if (row_ok) {
+#pragma unroll 1
+        for (int u = 0; u < nu; ++u) {
+          const float v = dot_q([&](int ch) { return urow(ch >> 3, u, ch); });
+#pragma unroll
+          for (int w = 0; w < kMaxU; ++w)
+            if (w == u) tu[w] = v;
+        }
+      }
+    }
+    float m_tot = (T > 0) ? m_ref : -INFINITY;
+    if (row_ok) {
+#pragma unroll
+      for (int u = 0; u < kMaxU; ++u) m_tot = fmaxf(m_tot, tu[u]);
+    }
+    const __nv_bfloat16* vub = a.vu + (int64_t)req * a.u_req_stride + (int64_t)b * a.u_beam_stride;
+    const float w_sh = (T > 0) ? ex2(m_ref - m_tot) : 0.f;
+    float den = l * w_sh;
+    float wu[kMaxU];
+#pragma unroll
+    for (int u = 0; u < kMaxU; ++u) {
+      wu[u] = (row_ok && u < nu) ? ex2(tu[u] - m_tot) : 0.f;
+      den += wu[u];
+    }
+    const float inv = 1.f / den;
+    uint8_t* ost = smem + kOffV + t * 2 * kQPanel;   // this tile's output staging (V ring)
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      uint32_t o[32];
+      if (T > 0) {
+        tmem_ld32(tO + lane_base + 32 * k, o);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) o[c] = 0u;
+      }
+      float acc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(o[c]) * w_sh;
+      if (row_ok) {
+#pragma unroll
+        for (int u = 0; u < kMaxU; ++u) {
+          if (u < nu) {
+            const uint4* vr = reinterpret_cast<const uint4*>(vub + ((int64_t)u * a.hkv + kvh) * kD + 32 * k);
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) {
+              float vf[8];
+              bf16x8_to_f32(a.u_stage ? urow(2 + (k >> 1), u, (k & 1) * 4 + ch) : __ldg(vr + ch), vf);
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[8 * ch + e] = fmaf(wu[u], vf[e], acc[8 * ch + e]);
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int ch = (k & 1) * 4 + c;
+        *reinterpret_cast<uint4*>(ost + (k >> 1) * kQPanel + r * 128 + ((ch ^ (r & 7)) << 4)) =
+            make_uint4(pack_bf16(acc[8 * c] * inv, acc[8 * c + 1] * inv),
+                       pack_bf16(acc[8 * c + 2] * inv, acc[8 * c + 3] * inv),
+                       pack_bf16(acc[8 * c + 4] * inv, acc[8 * c + 5] * inv),
+                       pack_bf16(acc[8 * c + 6] * inv, acc[8 * c + 7] * inv));
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + t) : "memory");   // this tile's 4 softmax warps
+    if (r == 0) {
+      const int b0 = (2 * mp + t) * nb;
+      tma_store_4d(&tm_o, su32(ost), 0, kvh * a.G, b0, req);
+      tma_store_4d(&tm_o, su32(ost) + kQPanel, 64, kvh * a.G, b0, req);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    if (row_ok && a.lse) a.lse[qrow] = (m_tot + __log2f(den)) * 0.6931471805599453f;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
   }
 }
 
@@ -788,6 +1179,30 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
     const uint64_t str[3] = {(uint64_t)kD * 2, (uint64_t)hq * kD * 2, (uint64_t)bw * hq * kD * 2};
     const uint32_t box[4] = {64, (uint32_t)G, (uint32_t)(kBM / G), 1};
     if (!make_map(&to, out, dims, str, box)) return 1;
+  }
+  // fused mode: the two-Q-tile kernel (k_attn_pair) unless XGR_ATTN_IMPL=1 selects the one-tile one
+  static const int impl_env = getenv("XGR_ATTN_IMPL") ? atoi(getenv("XGR_ATTN_IMPL")) : 2;
+  if (!pm && impl_env == 2) {
+    a.u_stage = (n_unshared > 0 && !(a.dbg & 2) && 8 * nb * n_unshared * 128 <= (int)(pair::kKStages * 2 * pair::kKVPanel) &&
+                 (nb * n_unshared) % 8 == 0) ? 1 : 0;
+    memset(&tku, 0, sizeof(tku));
+    memset(&tvu, 0, sizeof(tvu));
+    if (a.u_stage) {
+      const uint64_t dims[5] = {(uint64_t)kD, (uint64_t)hkv, (uint64_t)n_unshared, (uint64_t)bw, (uint64_t)n_req};
+      const uint64_t str[4] = {(uint64_t)kD * 2, (uint64_t)hkv * kD * 2, (uint64_t)u_beam_stride * 2,
+                               (uint64_t)std::max<int64_t>(u_req_stride, 1) * 2};
+      const uint32_t box[5] = {64, 1, (uint32_t)n_unshared, (uint32_t)nb, 1};
+      if (!make_map_nd(&tku, ku, 5, dims, str, box) || !make_map_nd(&tvu, vu, 5, dims, str, box)) return 1;
+    }
+    CUtensorMap tk2, tv2;
+    const uint64_t dims[4] = {(uint64_t)kD, (uint64_t)hkv, (uint64_t)std::max(ls, 1), (uint64_t)n_req};
+    const uint64_t str[3] = {(uint64_t)kD * 2, (uint64_t)hkv * kD * 2, (uint64_t)std::max(ls, 1) * hkv * kD * 2};
+    const uint32_t box[4] = {64, 1, (uint32_t)pair::kBN, 1};
+    if (!make_map(&tk2, ks, dims, str, box) || !make_map(&tv2, vs, dims, str, box)) return 1;
+    const dim3 grid2((unsigned)((bw * G + 255) / 256), (unsigned)hkv, (unsigned)n_req);
+    cudaFuncSetAttribute(k_attn_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pair::kSmem);
+    k_attn_pair<<<grid2, pair::kThreads, pair::kSmem, stream>>>(tq, tk2, tv2, tku, tvu, to, a);
+    return cudaGetLastError() == cudaSuccess ? 0 : 2;
   }
   const dim3 grid((unsigned)((bw * G + kBM - 1) / kBM), (unsigned)hkv, (unsigned)n_req);
   if (pm) {

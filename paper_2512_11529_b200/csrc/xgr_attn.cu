@@ -1180,8 +1180,8 @@ int launch_attn_shared(const void* q, const void* ks, const void* vs, int ls, co
     const uint32_t box[4] = {64, (uint32_t)G, (uint32_t)(kBM / G), 1};
     if (!make_map(&to, out, dims, str, box)) return 1;
   }
-  // fused mode: the two-Q-tile kernel (k_attn_pair) unless XGR_ATTN_IMPL=1 selects the one-tile one
-  static const int impl_env = getenv("XGR_ATTN_IMPL") ? atoi(getenv("XGR_ATTN_IMPL")) : 2;
+  // fused mode: XGR_ATTN_IMPL=2 selects the two-Q-tile kernel (k_attn_pair; slower, kept for study)
+  static const int impl_env = getenv("XGR_ATTN_IMPL") ? atoi(getenv("XGR_ATTN_IMPL")) : 1;
   if (!pm && impl_env == 2) {
     a.u_stage = (n_unshared > 0 && !(a.dbg & 2) && 8 * nb * n_unshared * 128 <= (int)(pair::kKStages * 2 * pair::kKVPanel) &&
                  (nb * n_unshared) % 8 == 0) ? 1 : 0;

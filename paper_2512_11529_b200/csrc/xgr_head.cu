@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(WPB * 32) k_head(const __grid_constant__ StepA
                                                    int64_t ldw, const float* __restrict__ bias, int d,
                                                    float* __restrict__ clog) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * WPB + (threadIdx.x >> 5), req = blockIdx.y;
   if (b >= a.BW) return;

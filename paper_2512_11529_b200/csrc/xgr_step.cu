@@ -576,7 +576,7 @@ __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, c
 template <int T, int VPT>
 __global__ void __launch_bounds__(T) k_theta(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   __shared__ uint32_t s_bm[T * VPT / 8];
   __shared__ float s_red[T / 32], s_red2[T / 32], s_red3[T / 32];
   __shared__ uint32_t s_hist[4096];
@@ -727,7 +727,7 @@ __device__ void sparse_row_main(const StepArgs& a, int req, int b, float S, floa
 template <int T, int VPT>
 __global__ void __launch_bounds__(T) k_main(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   __shared__ uint32_t s_bm[T * VPT / 8];
   __shared__ float s_red[T / 32], s_red2[T / 32];
   __shared__ int s_redi[T / 32];
@@ -943,7 +943,7 @@ __device__ void topk_scan(const uint64_t* keys, int m, int K, int V, int BW, int
 template <int T, typename TI = float>
 __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   extern __shared__ __align__(16) uint64_t s_keys[];  // [cap] keys, then [2 * kMaxBW] candidates
   uint64_t* s_cand = s_keys + a.cap;
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
@@ -1050,7 +1050,7 @@ template <int T>
 __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a, const uint64_t* grec,
                                              const int32_t* grec_n) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   extern __shared__ __align__(16) uint64_t s_keys[];  // [nranks * BW] keys, then [2 * kMaxBW]
   __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
   __shared__ TopkScratch s_sc;
@@ -1089,7 +1089,7 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
 template <int T, bool ROOT, typename TI = float, bool CMP = false>
 __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   extern __shared__ __align__(16) uint64_t s_dynk[];  // [2 * kMaxBW] candidates, then the keys
   uint64_t* s_cand = s_dynk;
   uint64_t* s_keys = s_dynk + 2 * kMaxBW;

@@ -163,7 +163,7 @@ __device__ __forceinline__ int cisum(int v, int* part) {
 template <int CTR, int R0, int MODE = kModeNormal>
 __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   constexpr int NT = CTR * R0;
   extern __shared__ __align__(128) float s_dyn[];
   float* s_row = s_dyn;                                                   // [R0][32*CTR]
@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 template <int T, int NCH, typename TI = float>
 __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk
   constexpr int VPT = NCH * CH / 4;          // x[] holds 4 * VPT = NCH * CH tokens per thread
   constexpr int NW = T / 32;
@@ -643,7 +643,7 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
 template <int T>
 __global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepArgs a) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   constexpr int PER = kSeedBins / T;
   __shared__ uint32_t s_w[T / 32];
   __shared__ int s_bin;
@@ -712,7 +712,7 @@ template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename
 __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   pdl_wait();
-  pdl_trigger();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   constexpr int GT = 256;          // consumer threads per group
   constexpr int VT = GT * EPT;     // tokens per stage row
   constexpr int MW = VT / 32;      // mask words per stage

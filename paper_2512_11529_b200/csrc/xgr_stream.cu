@@ -1323,7 +1323,10 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
         launch_pdl(k_stream<32, 1, 2, 3>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, seeded);
     }
-  } else if (a.topk) {   // V > 8192 with per-beam Top-K: the capped histogram seed
+  } else if (a.topk || (g_seed_mode == 1 && a.Vl <= 16384 && !a.gstats)) {
+    // V in (8192, 16384]: the histogram seed over R0 rows, one CTA per seed row (capped per
+    // beam with Top-K). The two-row exact seed below left C4 requests with weak thresholds:
+    // 4.2K survivors per request on average and survivor-buffer overflows into the exact fallback.
     const int r0 = std::min(a.theta_rows, rows);
     if (r0 > 0) {
       launch_pdl(k_seed_hist<256, 16>, dim3(a.batch, r0), 256, 0, s, a);

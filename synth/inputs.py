@@ -149,6 +149,7 @@ def prefix_keyed_row(seed: int, request: int, prefix, vocab: int) -> np.ndarray:
 ATTN_CONFIGS = {
     "A1": dict(n_req=2, bw=4, hq=4, hkv=2, d=128, ls=70, nd=3),          # tiny parity case
     "A2": dict(n_req=16, bw=256, hq=32, hkv=8, d=128, ls=1024, nd=3),    # bench workload
+    "A3": dict(n_req=4, bw=512, hq=32, hkv=8, d=128, ls=3072, nd=3),     # BW 512, 3k prompt (L559-566)
 }
 
 

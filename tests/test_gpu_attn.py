@@ -147,6 +147,24 @@ def test_deterministic_and_beam_isolation():
     assert np.array_equal(a[0, others], c[0, others]) and not np.array_equal(a[0, 5], c[0, 5])
 
 
+def test_bw512_long_prompt_sampled():
+    """A3 (BW 512, prompt 3072: the paper's largest beam width and input length, PAPER.md
+    L559-566), sampled beams of every request against the oracle."""
+    import paper_2512_11529_b200 as xgr
+    c = ATTN_CONFIGS["A3"]
+    n_req, bw, hq, hkv, d, ls, nd = (c[k] for k in ("n_req", "bw", "hq", "hkv", "d", "ls", "nd"))
+    scale = 1.0 / math.sqrt(d)
+    q, ks, vs, ku, vu = make_attn_inputs(n_req, bw, hq, hkv, d, ls, nd, seed=77, sigma_q=2.0)
+    out, lse = _run_staged(xgr, q, ks, vs, ku, vu, 2, hkv, scale)
+    rng = np.random.default_rng(1)
+    for r in range(n_req):
+        beams = np.sort(rng.choice(bw, 4, replace=False))
+        ref, rlse = A.staged_attention(q[r][beams], ks[r], vs[r], ku[r][beams], vu[r][beams], 2, scale)
+        bnd = _bound(q[r][beams], ks[r], vs[r], ku[r][beams], vu[r][beams], 2, scale, ref)
+        assert np.all(np.abs(out[r][beams] - ref) <= bnd)
+        assert np.allclose(lse[r][beams], rlse, rtol=1e-5, atol=1e-5)
+
+
 def test_full_size_sampled():
     """A2 (bench workload: 16 requests x BW 256 x 32 heads, 8 KV heads, prompt 1024, step 3 with
     3 own tokens per beam) in the launch configuration the bench times; the oracle checks sampled

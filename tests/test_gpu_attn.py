@@ -67,6 +67,27 @@ def test_staged_matches_oracle(shape, sigma_q):
         assert np.allclose(lse[r], rlse, rtol=1e-5, atol=1e-5)
 
 
+@pytest.mark.parametrize("trial", range(12))
+def test_random_shapes(trial):
+    """Random shapes (prompt 0-400 tokens, 1-70 beams, G = 1-8, 1-4 KV heads, 0-3 own tokens)
+    through both epilogue paths (staged or per-thread unshared rows, depending on the shape)."""
+    import paper_2512_11529_b200 as xgr
+    rng = np.random.default_rng(9000 + trial)
+    G = int(rng.choice([1, 2, 4, 8])); hkv = int(rng.choice([1, 2, 4]))
+    bw = int(rng.integers(1, 71)); ls = int(rng.integers(0, 401)); nd = 3
+    n = int(rng.integers(0 if ls > 0 else 1, 4))
+    n_req = int(rng.integers(1, 3))
+    scale = 1.0 / math.sqrt(128)
+    q, ks, vs, ku, vu = make_attn_inputs(n_req, bw, G * hkv, hkv, 128, ls, nd, seed=trial,
+                                         sigma_q=float(rng.choice([1.0, 3.0])))
+    out, lse = _run_staged(xgr, q, ks, vs, ku, vu, n, hkv, scale)
+    for r in range(n_req):
+        ref, rlse = A.staged_attention(q[r], ks[r], vs[r], ku[r], vu[r], n, scale)
+        bnd = _bound(q[r], ks[r], vs[r], ku[r], vu[r], n, scale, ref)
+        assert np.all(np.abs(out[r] - ref) <= bnd), (trial, G, hkv, bw, ls, n)
+        assert np.allclose(lse[r], rlse, rtol=1e-5, atol=1e-5)
+
+
 @pytest.mark.parametrize("n", [1, 2, 3])
 def test_empty_prompt_unshared_only(n):
     """ls = 0: the shared stage is the empty partial; output = unshared attention."""

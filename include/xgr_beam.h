@@ -204,9 +204,14 @@ xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_byte
  *   2. all-gather the stats of every rank, rank-major: gstats [G][batch][BW][2].
  *   3. xgr_shard_select: global lse per row = fixed rank-order combine of the G pairs (identical
  *      on every rank, R20); theta-pruned local top-BW of this rank's candidates.
- *      *recs: device uint64 keys [batch][BW] (0-padded), *rec_n: device int32 [batch].
- *   4. all-gather both: grecs [G][batch][BW], grec_n [G][batch].
+ *      *recs: device uint64 keys [batch][BW], sorted descending and 0-padded (no real key is 0),
+ *      *rec_n: device int32 [batch] (the count of nonzero keys).
+ *   4. all-gather the records: grecs [G][batch][BW] (and, optionally, grec_n [G][batch]).
  *   5. xgr_shard_merge: global top-BW of the union, committed identically on every rank.
+ *      grec_n may be NULL: the merge then counts each rank's nonzero keys itself, so a step needs
+ *      only two collectives (stats, records).
+ * xgr_beam_init rejects (XGR_ERR_UNSUPPORTED) an nranks x beam_width the merge's shared memory
+ * cannot hold on the device.
  * logits: this rank's columns only, [batch][rows][ld] with ld >= V/G; it must stay valid until
  * xgr_shard_select has completed on the stream. xgr_beam_step returns XGR_ERR_SEQUENCE on a
  * sharded ctx; finalize / view / history are unchanged. All calls only enqueue. */

@@ -285,13 +285,3 @@ def state_from_history(parent_hist, token_hist, scores, n_live) -> BeamState:
                      parents=np.asarray(parent_hist[-1][: int(n_live)], dtype=np.int64) if t else np.zeros(0, np.int64),
                      tokens=np.asarray(token_hist[-1][: int(n_live)], dtype=np.int64) if t else np.zeros(0, np.int64))
 
-
-def run_batch_step(vocab: Vocabulary, states, logits, bw: int, threads: int = 1):
-    """beam_step over a batch of requests; logits [batch][rows][ld]. Requests are independent,
-    so they may run on a thread pool (numpy releases the GIL in its kernels)."""
-    if threads <= 1 or len(states) <= 1:
-        return [beam_step(vocab, s, logits[r], bw) for r, s in enumerate(states)]
-    from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=threads) as ex:
-        futs = [ex.submit(beam_step, vocab, s, logits[r], bw) for r, s in enumerate(states)]
-        return [f.result() for f in futs]

@@ -6,6 +6,7 @@ the library and raises if it is missing: there is no CPU fallback.
 """
 from .binding import (  # noqa: F401
     BeamSearch,
+    ShardedBeamSearch,
     XgrConfig,
     XgrError,
     XGR_CFG_COUNTERS,

@@ -301,10 +301,12 @@ class BeamSearch:
         return (_view(r.value, (self.batch, self.bw), "<i8", self.device),
                 _view(n.value, (self.batch,), "<i4", self.device))
 
-    def shard_merge(self, grecs, grec_n, stream=None):
-        """grecs int64 [nranks][batch][BW], grec_n int32 [nranks][batch] (all ranks, rank-major)."""
+    def shard_merge(self, grecs, grec_n=None, stream=None):
+        """grecs int64 [nranks][batch][BW] (all ranks, rank-major); grec_n int32 [nranks][batch] or
+        None (the merge counts each rank's nonzero keys: no third collective)."""
         _check(lib.xgr_shard_merge(self.ctx, ctypes.c_void_p(grecs.data_ptr()),
-                                   ctypes.c_void_p(grec_n.data_ptr()), self._stream(stream)))
+                                   ctypes.c_void_p(0 if grec_n is None else grec_n.data_ptr()),
+                                   self._stream(stream)))
         self.t += 1
         self._shard_logits = None
 
@@ -534,12 +536,12 @@ class ShardedBeamSearch:
         return out.view(self.bs.nranks, *t.shape)
 
     def step(self, logits_local, stream=None):
+        """One decode step: two collectives (8 B per row of stats, 8 B per record)."""
         stats = self.bs.shard_stats(logits_local, stream)
         gstats = self._ag(stats)
-        recs, n = self.bs.shard_select(gstats, stream)
+        recs, _ = self.bs.shard_select(gstats, stream)
         grecs = self._ag(recs)
-        gn = self._ag(n)
-        self.bs.shard_merge(grecs, gn, stream)
+        self.bs.shard_merge(grecs, None, stream)
 
     def finalize(self, **kw):
         return self.bs.finalize(**kw)

@@ -22,6 +22,7 @@ cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s);
 cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches);
 cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
                                cudaStream_t s);
+cudaError_t merge_fits(int nranks, int bw, int device, bool* ok);
 cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
                             int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s);
 cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched,
@@ -178,6 +179,13 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   ACK(cudaGetDeviceCount(&ndev));
   if (c.device < 0 || c.device >= ndev) return fail(XGR_ERR_INVALID_ARG, "init: bad device %d", c.device);
   ACK(cudaSetDevice(c.device));
+  if (c.nranks > 1) {
+    bool ok = false;
+    ACK(merge_fits(c.nranks, c.beam_width, c.device, &ok));
+    if (!ok)
+      return fail(XGR_ERR_UNSUPPORTED, "init: the shard merge of nranks x beam_width = %d keys exceeds shared memory",
+                  c.nranks * c.beam_width);
+  }
 
   xgr_ctx* x = new xgr_ctx();
   x->cfg = c;
@@ -480,7 +488,7 @@ xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, con
 }
 
 xgr_status xgr_shard_merge(xgr_ctx* ctx, const uint64_t* grecs, const int32_t* grec_n, void* stream) {
-  if (!ctx || !grecs || !grec_n) return fail(XGR_ERR_INVALID_ARG, "shard_merge: NULL argument");
+  if (!ctx || !grecs) return fail(XGR_ERR_INVALID_ARG, "shard_merge: NULL argument");
   if (ctx->shard_phase != 2) return fail(XGR_ERR_SEQUENCE, "shard_merge: call shard_select first");
   StepArgs a = ctx->shard_args;
   a.stats_out = nullptr;

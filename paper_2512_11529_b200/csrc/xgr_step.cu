@@ -1056,17 +1056,33 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
   __shared__ TopkScratch s_sc;
   __shared__ ParentInfo s_pi;
   __shared__ int s_off[65];
-  const int req = blockIdx.x, tid = threadIdx.x;
+  __shared__ int s_cnt[64];
+  const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
   uint64_t* s_cand = s_keys + (size_t)a.nranks * a.BW;
+  if (grec_n) {
+    if (tid < a.nranks) s_cnt[tid] = grec_n[tid * a.batch + req];
+  } else {
+    // no counts exchanged: each rank's records are sorted descending and 0-padded, and no real key
+    // is 0 (its score half is orderable(c) != 0 for every c, -inf included), so the count is the
+    // number of nonzero keys -- one warp per rank
+    for (int g = tid >> 5; g < a.nranks; g += T / 32) {
+      const uint64_t* src = grec + ((size_t)g * a.batch + req) * a.BW;
+      int c = 0;
+      for (int i = lane; i < a.BW; i += 32) c += src[i] != 0ull;
+      c = __reduce_add_sync(0xffffffffu, c);
+      if (lane == 0) s_cnt[g] = c;
+    }
+  }
+  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
+  __syncthreads();
   if (tid == 0) {
     int o = 0;
     for (int g = 0; g < a.nranks; ++g) {
       s_off[g] = o;
-      o += grec_n[g * a.batch + req];
+      o += s_cnt[g];
     }
     s_off[a.nranks] = o;
   }
-  prefetch_parents<T>(a, req, nlive_of(a, req), s_pi);
   __syncthreads();
   const int n = s_off[a.nranks];
   for (int g = 0; g < a.nranks; ++g) {
@@ -1579,9 +1595,24 @@ cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int
   return cudaGetLastError();
 }
 
+static size_t merge_smem(int nranks, int bw) { return ((size_t)nranks * bw + 2 * kMaxBW) * sizeof(uint64_t); }
+
+// Whether k_merge's shared memory (nranks x BW keys + the selection scratch) fits the device's
+// opt-in limit; checked once at init so an oversized shard configuration fails there, not after
+// the stats and select phases of a step.
+cudaError_t merge_fits(int nranks, int bw, int device, bool* ok) {
+  int optin = 0;
+  cudaError_t e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (e != cudaSuccess) return e;
+  cudaFuncAttributes fa;
+  if ((e = cudaFuncGetAttributes(&fa, k_merge<512>)) != cudaSuccess) return e;
+  *ok = merge_smem(nranks, bw) + fa.sharedSizeBytes <= (size_t)optin;
+  return cudaSuccess;
+}
+
 cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
                                cudaStream_t s) {
-  const size_t smem = ((size_t)a.nranks * a.BW + 2 * kMaxBW) * sizeof(uint64_t);
+  const size_t smem = merge_smem(a.nranks, a.BW);
   cudaError_t e = cudaFuncSetAttribute(k_merge<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   launch_pdl(k_merge<512>, a.batch, 512, smem, s, a, grec, grec_n);

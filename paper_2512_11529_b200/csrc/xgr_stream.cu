@@ -517,11 +517,11 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
                    : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w) : "l"(row + CH * q));
   }
   const int nl = nlive_of(a, req);
+  if (r >= nl) return;   // before any beam-state read: r < theta_rows may exceed BW
   float S;
   uint32_t node;
   row_state(a, req, r, S, node);
   const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
-  if (r >= nl) return;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   if (slot < 0) return;   // sparse seed rows contribute nothing (no bound from them)
@@ -708,12 +708,25 @@ __device__ __forceinline__ uint64_t stage_mask(const uint32_t* msk, int lt) {
   }
 }
 
-template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float>
-__global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
+// Stage ring: NS stages, NSG = NS / G of them owned by each consumer group. Row k goes to group
+// g = k % G as that group's j-th row (j = k / G), in stage g + G * (j % NSG), phase j / NSG. A stage
+// is only ever used by one group, so a group's parity wait on it cannot be satisfied by a phase
+// that belongs to another group's row (a parity wait cannot tell phase n from phase n - 2).
+template <int G, int NS>
+struct Ring {
+  static_assert(NS % G == 0, "each consumer group owns NS / G stages");
+  static constexpr int NSG = NS / G;
+  __device__ static __forceinline__ int stage(int k) { return (k % G) + G * ((k / G) % NSG); }
+  __device__ static __forceinline__ int use(int k) { return (k / G) / NSG; }   // n-th use of the stage
+};
+
+template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float, int GT = 256>
+__global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   pdl_wait();
   if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
-  constexpr int GT = 256;          // consumer threads per group
+  // GT consumer threads per group (256, or 512 for 16384-token rows)
+  using R = Ring<G, NS>;
   constexpr int VT = GT * EPT;     // tokens per stage row
   constexpr int MW = VT / 32;      // mask words per stage
   constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk (4 fp32, 8 bf16)
@@ -825,10 +838,10 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
         const uint32_t jnode = __shfl_sync(0xffffffffu, m0.node, j);
         const float jlse = __shfl_sync(0xffffffffu, m0.lse, j);
         if (lane == 0) {
-          const int st = kj % NS;
-          if (kj >= NS) {
-            if (a.dbg & 4096) mbar_wait(&empty[st], ((kj / NS) - 1) & 1);
-            else mbar_wait_sleep(&empty[st], ((kj / NS) - 1) & 1);
+          const int st = R::stage(kj), u = R::use(kj);
+          if (u > 0) {   // the stage's previous row (same group) has been consumed
+            if (a.dbg & 4096) mbar_wait(&empty[st], (u - 1) & 1);
+            else mbar_wait_sleep(&empty[st], (u - 1) & 1);
           }
           Desc d;
           d.req = jreq;
@@ -905,10 +918,29 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
   for (int k = g;; k += G) {
     const int w = blockIdx.x + k * gridDim.x;
     if (w >= total) break;
-    const int st = k % NS;
-    mbar_wait(&full[st], (k / NS) & 1);
-    const Desc d = desc[st];
-    const float th = s_th[st];
+    const int st = R::stage(k);
+    mbar_wait(&full[st], R::use(k) & 1);
+    // lane 0 reads the row descriptor and broadcasts it: the thread that later releases the
+    // stage (the empty-barrier arrive) is then the one that read it
+    Desc d;
+    float th;
+    {
+      int4 di = make_int4(0, 0, 0, 0);
+      float4 df = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (lane == 0) {
+        const Desc& sd = desc[st];
+        di = make_int4(sd.req, sd.b, sd.kind, sd.slot);
+        df = make_float4(sd.S, __uint_as_float(sd.node), sd.lse, s_th[st]);
+      }
+      d.req = __shfl_sync(0xffffffffu, di.x, 0);
+      d.b = __shfl_sync(0xffffffffu, di.y, 0);
+      d.kind = __shfl_sync(0xffffffffu, di.z, 0);
+      d.slot = __shfl_sync(0xffffffffu, di.w, 0);
+      d.S = __shfl_sync(0xffffffffu, df.x, 0);
+      d.node = __float_as_uint(__shfl_sync(0xffffffffu, df.y, 0));
+      d.lse = __shfl_sync(0xffffffffu, df.z, 0);
+      th = __shfl_sync(0xffffffffu, df.w, 0);
+    }
     const int req = d.req, b = d.b;
     const float S = d.S;
 
@@ -1196,17 +1228,16 @@ __global__ void __launch_bounds__(256 * G + 32, MINB) k_stream(const __grid_cons
   flush();
 }
 
-template <int EPT, int NS, typename TI = float>
+template <int EPT, int NS, typename TI = float, int GT = 256>
 static size_t stream_smem() {
-  return (size_t)NS * (256 * EPT * sizeof(TI) + 256 * EPT / 8);
+  return (size_t)NS * (GT * EPT * sizeof(TI) + GT * EPT / 8);
 }
 
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
 static int g_seed_kernel = 0;      // XGR_SEED_KERNEL: 0 seed rows streamed (k_stream seed mode), 1 k_seed_hist
-static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed),
-                                   // 2 also the histogram seed for V in (8192, 16384]
+static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>
 static cudaError_t opt_in(K k, size_t smem) {
@@ -1223,15 +1254,17 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 3, 6>, stream_smem<32, 6>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 2, 3>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 1, 4>, stream_smem<32, 1>())) != cudaSuccess) return e;
-  if ((e = opt_in(k_stream<64, 2, 3>, stream_smem<64, 3>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 3, 1, kModeNormal, float, 512>, stream_smem<32, 3, float, 512>())) != cudaSuccess)
+    return e;
+  if ((e = opt_in(k_stream<32, 1, 4, 1, kModeNormal, __nv_bfloat16, 512>, stream_smem<32, 4, __nv_bfloat16, 512>())) !=
+      cudaSuccess)
+    return e;
   if ((e = opt_in(k_seed<256, 4>, stream_smem<32, 4>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 4, kModeShardEmit>, stream_smem<32, 4>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeStats>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeShardEmit>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_seed<256, 2>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 4, 3, kModeNormal, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) != cudaSuccess)
-    return e;
-  if ((e = opt_in(k_stream<64, 1, 3, 2, kModeNormal, __nv_bfloat16>, stream_smem<64, 3, __nv_bfloat16>())) != cudaSuccess)
     return e;
   if (const char* v = getenv("XGR_SEED_ROWS")) g_seed_rows = atoi(v);
   if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
@@ -1284,11 +1317,11 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     if (ev0) cudaEventRecord(ev0, s);
     if (a.trie.V <= 8192)
-      launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s, 
+      launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s,
           a, total, 0);
-    else
-      launch_pdl(k_stream<64, 1, 3, 2, kModeNormal, bf>, std::min(total, 2 * sms), 256 + 32, stream_smem<64, 3, bf>(), s, 
-          a, total, 0);
+    else   // 16384-token rows: one 512-thread consumer group per SM, 4 x 32 KB stages
+      launch_pdl(k_stream<32, 1, 4, 1, kModeNormal, bf, 512>, std::min(total, sms), 512 + 32,
+                 stream_smem<32, 4, bf, 512>(), s, a, total, 0);
     if (ev1) cudaEventRecord(ev1, s);
     *launches += 2;
     return cudaGetLastError();
@@ -1324,24 +1357,26 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
         launch_pdl(k_stream<32, 1, 2, 3>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, seeded);
     }
-  } else if (a.topk || (g_seed_mode == 2 && a.Vl <= 16384 && !a.gstats)) {
-    // V in (8192, 16384]: the histogram seed over R0 rows, one CTA per seed row (capped per beam
-    // with Top-K). XGR_SEED_MODE=2 selects it without Top-K: C4 passes take 4.4 instead of
-    // 22.6 ms (the two-row exact seed below leaves weak thresholds and survivor overflows), but
-    // the C4 full-size test faults after the rest of the GPU suite in that mode (not yet found),
-    // so it is not the default.
-    const int r0 = std::min(a.theta_rows, rows);
-    if (r0 > 0) {
-      launch_pdl(k_seed_hist<256, 16>, dim3(a.batch, r0), 256, 0, s, a);
-      ++*launches;
-    }
-    launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
-    if (ev0) cudaEventRecord(ev0, s);
-    launch_pdl(k_stream<64, 2, 3>, grid, 2 * 256 + 32, stream_smem<64, 3>(), s, a, total, 0);
   } else {
-    launch_pdl(k_seed<512, 2>, a.batch, 1024, stream_smem<64, 2>(), s, a);
-    if (ev0) cudaEventRecord(ev0, s);
-    launch_pdl(k_stream<64, 2, 3>, grid, 2 * 256 + 32, stream_smem<64, 3>(), s, a, total, 2);
+    // V in (8192, 16384]: the histogram seed over R0 rows (one CTA per seed row, capped per beam
+    // with Top-K), then 64 KB rows streamed by one 512-thread consumer group per SM (3 stages).
+    // XGR_SEED_MODE=0 selects the exact two-row union seed (k_seed<512, 2>; weaker thresholds).
+    if (g_seed_mode >= 1 || a.topk || a.gstats) {
+      const int r0 = std::min(a.theta_rows, rows);
+      if (r0 > 0) {
+        launch_pdl(k_seed_hist<256, 16>, dim3(a.batch, r0), 256, 0, s, a);
+        ++*launches;
+      }
+      launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
+      if (ev0) cudaEventRecord(ev0, s);
+      launch_pdl(k_stream<32, 1, 3, 1, kModeNormal, float, 512>, std::min(total, sms), 512 + 32,
+                 stream_smem<32, 3, float, 512>(), s, a, total, 0);
+    } else {
+      launch_pdl(k_seed<512, 2>, a.batch, 1024, stream_smem<64, 2>(), s, a);
+      if (ev0) cudaEventRecord(ev0, s);
+      launch_pdl(k_stream<32, 1, 3, 1, kModeNormal, float, 512>, std::min(total, sms), 512 + 32,
+                 stream_smem<32, 3, float, 512>(), s, a, total, 2);
+    }
   }
   if (ev1) cudaEventRecord(ev1, s);
   *launches += 2;

@@ -14,6 +14,7 @@ from .inputs import (  # noqa: F401
     make_items,
     make_logits,
     make_logits_torch,
+    make_logits_rows_torch,
     prefix_keyed_row,
     ATTN_CONFIGS,
     to_bf16_grid,

@@ -126,6 +126,26 @@ def make_logits_torch(shape, seed: int, sigma: float = 2.0, device="cuda"):
     return x
 
 
+def make_logits_rows_torch(requests, rows: int, vocab: int, step: int, key: int, sigma: float = 2.0,
+                           col0: int = 0, ncols: int | None = None, device="cuda"):
+    """fp32 N(0, sigma^2) logits [len(requests)][rows][ncols] whose values depend only on (key, step,
+    request, column): request r's full [rows][vocab] block comes from its own torch Philox stream,
+    and columns [col0, col0 + ncols) are kept. A request therefore sees the same bytes however the
+    batch is split across ranks (request split) or the columns across shards (codebook shard)."""
+    import torch
+    ncols = vocab - col0 if ncols is None else ncols
+    out = torch.empty((len(requests), rows, ncols), dtype=torch.float32, device=device)
+    g = torch.Generator(device=device)
+    for i, r in enumerate(requests):
+        seed = splitmix64((key + 0x9E3779B97F4A7C15 * (step + 1) + 0x632BE59BD9B4E019 * (int(r) + 1))
+                          & 0xFFFFFFFFFFFFFFFF)
+        g.manual_seed(seed & 0x7FFFFFFFFFFFFFFF)
+        x = torch.randn((rows, vocab), generator=g, device=device, dtype=torch.float32)
+        out[i].copy_(x[:, col0:col0 + ncols])
+        out[i].mul_(float(sigma))
+    return out
+
+
 def prefix_keyed_row(seed: int, request: int, prefix, vocab: int) -> np.ndarray:
     """fp32 row x(prefix, v) for v < vocab: Irwin-Hall(4) of 16-bit fields of a splitmix64 hash,
     scaled by 2^-15 (exact). Same prefix -> same row, whatever slot it sits in."""

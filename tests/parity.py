@@ -31,7 +31,8 @@ class ParityFailure(AssertionError):
 def compare_step(voc, state, logits_r, bw, g_par, g_tok, g_score, g_nlive, where="", top_k=None):
     """Returns 'strict' or 'adjudicated'; raises ParityFailure otherwise."""
     c, flat, b, v, nonfinite = O.step_candidates(voc, state, logits_r)
-    c_all, b_all, v_all = c, b, v
+    c_all, flat_all = c, flat          # flat is ascending (rows in slot order, tokens sorted)
+    V = voc.vocab
     rowcut = {}
     if top_k is not None and top_k < bw:
         keep = O.per_beam_topk(c, flat, b, top_k)
@@ -44,37 +45,69 @@ def compare_step(voc, state, logits_r, bw, g_par, g_tok, g_score, g_nlive, where
     n_o = len(sel)
     if int(g_nlive) != n_o:
         raise ParityFailure(f"{where}: n_live gpu {g_nlive} != oracle {n_o}")
-    o_pairs = list(zip(b[sel].tolist(), v[sel].tolist()))
-    g_pairs = list(zip(np.asarray(g_par[:n_o]).tolist(), np.asarray(g_tok[:n_o]).tolist()))
-    c64 = {(int(bb), int(vv)): float(cc) for bb, vv, cc in zip(b_all, v_all, c_all)}
-    gs = np.asarray(g_score[:n_o], dtype=np.float64)
+    o_flat = flat[sel]
+    gp = np.asarray(g_par[:n_o], dtype=np.int64)
+    gt = np.asarray(g_tok[:n_o], dtype=np.int64)
     # dead slots
     if np.any(np.asarray(g_par[n_o:]) != -1) or np.any(np.asarray(g_tok[n_o:]) != -1):
         raise ParityFailure(f"{where}: dead slots not (-1, -1)")
     if np.any(~np.isneginf(np.asarray(g_score[n_o:], dtype=np.float64))):
         raise ParityFailure(f"{where}: dead slot scores not -inf")
-    for j, p in enumerate(g_pairs):
-        if p not in c64:
-            raise ParityFailure(f"{where}: slot {j} pair {p} is not a legal candidate")
-        if abs(gs[j] - c64[p]) > tol(c64[p]):
-            raise ParityFailure(f"{where}: slot {j} score {gs[j]!r} vs fp64 {c64[p]!r}")
-    if g_pairs == o_pairs:
+    # every GPU pair must be a legal candidate (b < n_live, v among the children of b's prefix)
+    g_flat = gp * V + gt
+    ok = (gp >= 0) & (gp < state.n_live) & (gt >= 0) & (gt < V)
+    pos = np.clip(np.searchsorted(flat_all, g_flat), 0, max(len(flat_all) - 1, 0))
+    ok &= flat_all[pos] == g_flat
+    if not np.all(ok):
+        j = int(np.argmin(ok))
+        raise ParityFailure(f"{where}: slot {j} pair {(int(gp[j]), int(gt[j]))} is not a legal candidate")
+    g_c64 = c_all[pos]                   # fp64 recompute of each GPU selection
+    gs = np.asarray(g_score[:n_o], dtype=np.float64)
+    tol_v = 1e-5 * np.maximum(1.0, np.abs(g_c64))
+    bad = ~(np.abs(gs - g_c64) <= tol_v)
+    if np.any(bad):
+        j = int(np.argmax(bad))
+        raise ParityFailure(f"{where}: slot {j} score {gs[j]!r} vs fp64 {g_c64[j]!r}")
+    if np.array_equal(g_flat, o_flat):
         return "strict"
-    theta64 = c64[o_pairs[-1]]
-    for p in set(g_pairs) ^ set(o_pairs):
-        cut = rowcut.get(p[0])
-        if abs(c64[p] - theta64) > tol(theta64) and (cut is None or abs(c64[p] - cut) > tol(cut)):
-            raise ParityFailure(f"{where}: set differs at {p} (c64 {c64[p]!r}, theta64 {theta64!r})")
+    theta64 = float(c[sel][-1])
+
+    def c64_of(f):
+        return float(c_all[np.searchsorted(flat_all, f)])
+
+    for f in set(g_flat.tolist()) ^ set(o_flat.tolist()):
+        cc = c64_of(f)
+        cut = rowcut.get(f // V)
+        if abs(cc - theta64) > tol(theta64) and (cut is None or abs(cc - cut) > tol(cut)):
+            raise ParityFailure(f"{where}: set differs at {(f // V, f % V)} (c64 {cc!r}, theta64 {theta64!r})")
     for j in range(n_o - 1):
-        a, bnext = c64[g_pairs[j]], c64[g_pairs[j + 1]]
+        a, bnext = g_c64[j], g_c64[j + 1]
         if bnext > a + tol(a):
             raise ParityFailure(f"{where}: order inversion at slot {j}")
-        if bnext == a:
-            fa = g_pairs[j][0] * voc.vocab + g_pairs[j][1]
-            fb = g_pairs[j + 1][0] * voc.vocab + g_pairs[j + 1][1]
-            if not fa < fb:
-                raise ParityFailure(f"{where}: tie order at slot {j}")
+        if bnext == a and not g_flat[j] < g_flat[j + 1]:
+            raise ParityFailure(f"{where}: tie order at slot {j}")
     return "adjudicated"
+
+
+def compare_many(voc, states, logits_fn, bw, par, tok, sc, nl, reqs, where="", top_k=None, threads=None):
+    """compare_step over many requests on a thread pool (numpy releases the GIL in its kernels).
+    states: {r: BeamState}; logits_fn(r) -> that request's [rows][ld] logits (fp32 numpy).
+    Returns {'strict': n, 'adjudicated': n, 'adjudicated_at': [(r, ...)]}."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+    threads = threads or min(32, max(1, len(os.sched_getaffinity(0))))
+
+    def one(r):
+        return r, compare_step(voc, states[r], logits_fn(r), bw, par[r], tok[r], sc[r], nl[r],
+                               where=f"{where} req {r}", top_k=top_k)
+
+    out = {"strict": 0, "adjudicated": 0, "adjudicated_at": []}
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        for r, res in ex.map(one, reqs):
+            out[res] += 1
+            if res == "adjudicated":
+                out["adjudicated_at"].append(r)
+    return out
 
 
 def gpu_states(hist_par, hist_tok, scores, nlive):

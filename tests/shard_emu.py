@@ -21,9 +21,9 @@ class ShardEmulator:
         gstats = torch.stack([s.clone() for s in stats]).contiguous()
         outs = [bs.shard_select(gstats) for bs in self.ranks]
         grecs = torch.stack([r.clone() for r, _ in outs]).contiguous()
-        gn = torch.stack([n.clone() for _, n in outs]).contiguous()
+        # two exchanges per step (stats, records): the merge counts each rank's nonzero records
         for bs in self.ranks:
-            bs.shard_merge(grecs, gn)
+            bs.shard_merge(grecs, None)
         for bs in self.ranks:
             bs.batch = logits_full.shape[0]
         torch.cuda.synchronize()

@@ -1,5 +1,5 @@
 """C5 at full size: 1B-item trie, V = 65536, BW = 512, batch 128, ND = 3, codebook-sharded over
-G = 8 rank contexts (8192 columns each) emulated on one GPU (tests/shard_emu.py), sampled requests
+G = 8 rank contexts (8192 columns each) emulated on one GPU (tests/shard_emu.py), every request
 checked against the teacher-forced oracle at every step, every rank's state bitwise identical.
 
 Heavy-ish: 1B items (~50 GB host RAM peak for the generator and the oracle's sorted key list),
@@ -18,7 +18,7 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow,
 
 from oracle import xbeam_oracle as O  # noqa: E402
 from synth import config, make_items, make_logits_torch  # noqa: E402
-from tests.parity import compare_step  # noqa: E402
+from tests.parity import compare_many  # noqa: E402
 from tests.shard_emu import ShardEmulator  # noqa: E402
 
 
@@ -28,7 +28,7 @@ def test_c5_full_size_codebook_shard():
     import paper_2512_11529_b200 as xgr
     c = config("C5")
     V, nd, bw, B, G = c["vocab"], c["nd"], c["beam_width"], c["batch"], 8
-    check = [0, 64, 127]
+    check = list(range(B))
     t0 = time.time()
     items = make_items(c["n_items"], V, nd, c["trie_key"])
     t_gen = time.time() - t0
@@ -61,9 +61,10 @@ def test_c5_full_size_codebook_shard():
             assert np.array_equal(v["parent"].cpu().numpy(), par)
             assert np.array_equal(v["token"].cpu().numpy(), tok)
             assert np.array_equal(v["score"].cpu().numpy(), sc)
-        for r in check:
-            res[compare_step(voc, states[r], x[r].cpu().numpy(), bw, par[r], tok[r], sc[r], nl[r],
-                             where=f"C5 req {r} step {t + 1}")] += 1
+        cm = compare_many(voc, states, lambda r: x[r].cpu().numpy(), bw, par, tok, sc, nl, check,
+                          where=f"C5 step {t + 1}", threads=16)
+        res["strict"] += cm["strict"]
+        res["adjudicated"] += cm["adjudicated"]
         hist_p.append(par)
         hist_t.append(tok)
         del x
@@ -76,5 +77,6 @@ def test_c5_full_size_codebook_shard():
         for j in range(bw):
             tup = tuple(int(a) for a in outs[0]["tokens"][r, j])
             assert voc.item_rank(tup) == int(outs[0]["item_rank"][r, j])
+    assert res["adjudicated"] <= max(2, (res["strict"] + res["adjudicated"]) // 100), res
     print(f"\nC5 full: items {t_gen:.1f} s, oracle vocabulary {t_voc:.1f} s, 8 tries {t_build:.1f} s, "
           f"steps {['%.2f s' % s for s in t_steps]} (untimed emulation), checks {res}")

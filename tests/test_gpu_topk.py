@@ -98,3 +98,12 @@ def test_topk_overflow_fallback(xgr):
                 states[r] = O.beam_step(voc, states[r], xs[t][r], bw, top_k=k)
         assert bs.counters()["overflow"] > 0
         bs.finalize(on_device=True)
+
+
+@pytest.mark.parametrize("k", [1, 50])
+def test_topk_v16384_many_rows_per_cta(xgr, k):
+    """V = 16384 with per-beam Top-K (the histogram seed + 512-thread streaming kernel) and far more
+    rows than CTAs (8 x 512 rows on 148 SMs), peaky logits so skipped and streamed rows interleave."""
+    vocab, nd, bw, batch = 16384, 3, 512, 8
+    items = make_items(20_000_000, vocab, nd, 161616)
+    _check(xgr, items, vocab, nd, bw, batch, k, flags=2, sigma=4.0, seed=k, check=[0, 3, 7])

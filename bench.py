@@ -236,9 +236,7 @@ def paper_heap_sample(voc, cfg, logits_fn, n_req: int, threads: int):
         from oracle import paper_heap_c
     except (ImportError, OSError):
         return None
-    import numpy as np
-    lg = [np.stack([logits_fn(r, t) if t else np.broadcast_to(logits_fn(r, 0), (cfg["beam_width"], cfg["vocab"]))
-                    for t in range(cfg["nd"])]) for r in range(n_req)]
+    lg = [[logits_fn(r, t) for t in range(cfg["nd"])] for r in range(n_req)]
     runner = paper_heap_c.PaperHeap(voc.keys, cfg["vocab"], cfg["nd"])
     t0 = time.perf_counter()
     stats = runner.run(lg, cfg["beam_width"], threads)

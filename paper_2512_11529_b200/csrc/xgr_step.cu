@@ -1450,6 +1450,7 @@ __global__ void k_children(TrieDev tr, const int32_t* prefixes, int depth, int64
 // ---------------------------------------------------------------------------------------------
 __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
                           unsigned long long* out /* alg, full, legal */) {
+  // this rank's columns [c0, c0 + Vl): the whole row unless codebook-sharded
   const int req = blockIdx.x, b = blockIdx.y;
   const int nl = nlive_of(a, req);
   if (b >= nl) return;
@@ -1460,32 +1461,38 @@ __global__ void k_account(const __grid_constant__ StepArgs a, uint32_t* touched,
   row_state(a, req, b, S, node);
   const LevelDev& L = a.trie.lv[a.level];
   const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
-  const int V = a.trie.V;
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  const int c0 = a.col0, Vl = a.Vl;
   const int esz = a.dtype == XGR_DTYPE_BF16 ? 2 : 4;   // bytes per logit; a 32-B sector holds 32/esz
-  if (threadIdx.x == 0) {
-    atomicAdd(out + 1, (unsigned long long)V * (unsigned long long)esz);
-    atomicAdd(out + 2, (unsigned long long)(fe - fc));
-  }
+  uint32_t nleg = 0;   // legal children in this rank's columns
+  for (uint32_t k2 = fc + threadIdx.x; k2 < fe; k2 += blockDim.x)
+    nleg += (lab[k2] >= (uint32_t)c0 && lab[k2] < (uint32_t)(c0 + Vl)) ? 1u : 0u;
+  nleg = __reduce_add_sync(0xffffffffu, nleg);
+  if (lane_id() == 0 && nleg) atomicAdd(out + 2, (unsigned long long)nleg);
+  if (threadIdx.x == 0) atomicAdd(out + 1, (unsigned long long)Vl * (unsigned long long)esz);
   if (S < thstar) return;  // a row the method need not read
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
   unsigned long long bytes = 0;
   if (slot >= 0) {
     if (esz == 4) {   // 8 tokens per sector: one bitmap byte
-      const uint8_t* bm = reinterpret_cast<const uint8_t*>(L.bitmap + (size_t)slot * a.trie.W);
-      for (int s = threadIdx.x; s < (V + 7) / 8; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+      const uint8_t* bm = reinterpret_cast<const uint8_t*>(L.bitmap + (size_t)slot * a.trie.W) + c0 / 8;
+      for (int s2 = threadIdx.x; s2 < (Vl + 7) / 8; s2 += blockDim.x) bytes += bm[s2] ? 32ull : 0ull;
     } else {          // 16 tokens per sector: one bitmap half-word
-      const uint16_t* bm = reinterpret_cast<const uint16_t*>(L.bitmap + (size_t)slot * a.trie.W);
-      for (int s = threadIdx.x; s < (V + 15) / 16; s += blockDim.x) bytes += bm[s] ? 32ull : 0ull;
+      const uint16_t* bm = reinterpret_cast<const uint16_t*>(L.bitmap + (size_t)slot * a.trie.W) + c0 / 16;
+      for (int s2 = threadIdx.x; s2 < (Vl + 15) / 16; s2 += blockDim.x) bytes += bm[s2] ? 32ull : 0ull;
     }
     if (threadIdx.x == 0) {
       uint32_t old = atomicOr(touched + (slot >> 5), 1u << (slot & 31));
-      if (!((old >> (slot & 31)) & 1u)) bytes += (unsigned long long)((V + 7) / 8);
+      if (!((old >> (slot & 31)) & 1u)) bytes += (unsigned long long)((Vl + 7) / 8);
       bytes += 16;
     }
   } else {
-    const uint16_t* lab = a.trie.lv[a.level + 1].label;
-    for (uint32_t k2 = fc + threadIdx.x; k2 < fe; k2 += blockDim.x)
-      if (k2 == fc || (lab[k2] * esz) / 32 != (lab[k2 - 1] * esz) / 32) bytes += 32;
+    for (uint32_t k2 = fc + threadIdx.x; k2 < fe; k2 += blockDim.x) {
+      const uint32_t v = lab[k2];
+      if (v < (uint32_t)c0 || v >= (uint32_t)(c0 + Vl)) continue;
+      if (k2 == fc || lab[k2 - 1] < (uint32_t)c0 || ((v - c0) * esz) / 32 != ((lab[k2 - 1] - c0) * esz) / 32)
+        bytes += 32;
+    }
     if (threadIdx.x == 0) bytes += 4 + 2ull * (fe - fc) + 16;
   }
   bytes = __reduce_add_sync(0xffffffffu, (unsigned)bytes);

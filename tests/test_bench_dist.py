@@ -34,7 +34,15 @@ def _worker(rank, world, port, q):
     seeds = bench.step_seeds(plan, cfg["nd"])
     t = bench.max_over_ranks(float(10 + rank), world, device=torch.device("cpu"))
     bench.barrier(world)
-    q.put((rank, plan, seeds, t, bench.candidates_per_pass(cfg, plan["batch"])))
+    # C4 request split and C5 codebook shard plans, and the shard exchange's rank-major layout
+    c4, c5 = config("C4"), config("C5")
+    p4 = bench.rank_plan(c4, rank, world, bench.split_mode(c4))
+    p5 = bench.rank_plan(c5, rank, world, bench.split_mode(c5))
+    L = p5["shards"][1] - p5["shards"][0]
+    local = torch.stack([torch.full((3, 2), float(g)) for g in range(*p5["shards"])])   # [L][...]
+    gathered = bench.shard_all_gather(local, world)
+    q.put((rank, plan, seeds, t, bench.candidates_per_pass(cfg, plan["batch"]), p4, p5, L,
+           gathered[:, 0, 0].tolist(), bench.pass_candidates(c4, p4, world), bench.pass_candidates(c5, p5, world)))
     dist.destroy_process_group()
 
 
@@ -50,11 +58,19 @@ def test_two_ranks_gloo():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    (r0, p0, s0, t0, c0), (r1, p1, s1, t1, c1) = res
+    (r0, p0, s0, t0, c0, a4, a5, L0, g0, n4, n5), (r1, p1, s1, t1, c1, b4, b5, L1, g1, m4, m5) = res
     assert t0 == t1 == 11.0                     # max over ranks
     assert set(s0).isdisjoint(s1)               # distinct logit seeds per rank
     assert p0["requests"][1] == p1["requests"][0]   # contiguous, disjoint request ranges
     assert p0["batch"] == p1["batch"] == 256 and c0 == c1 == 256 * (1 + 256 * 2) * 8192
+    # C4 strong split: 256 + 256 of the 512 requests, whole-job candidates counted once
+    assert a4["mode"] == "strong" and a4["requests"] == (0, 256) and b4["requests"] == (256, 512)
+    assert n4 == m4 == 512 * (1 + 512 * 3) * 16384
+    # C5 codebook shard: 4 + 4 of the 8 shards; every rank holds the whole batch; the all-gather
+    # returns the 8 shards in global order on both ranks
+    assert a5["shards"] == (0, 4) and b5["shards"] == (4, 8) and L0 == L1 == 4
+    assert g0 == g1 == [float(g) for g in range(8)]
+    assert n5 == m5 == 128 * (1 + 512 * 2) * 65536
 
 
 def test_reference_arm_nonzero_rank_exits(monkeypatch):

@@ -44,6 +44,7 @@ struct xgr_ctx {
   int32_t** d_phist = nullptr;     // device array of nd pointers
   int32_t** d_thist = nullptr;
   uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
+  uint32_t* next_keys[2] = {nullptr, nullptr};   // per-request next-step candidates (route), by step parity
   uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
   float* head_logits = nullptr;    // [maxB][kSparseCap]: legal logits of a fused-head sparse step
   uint64_t* surv = nullptr;        // [maxB][cap]
@@ -118,6 +119,8 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->d_phist);
   cudaFree(c->d_thist);
   cudaFree(c->scratch);
+  cudaFree(c->next_keys[0]);
+  cudaFree(c->next_keys[1]);
   cudaFree(c->seed_hist);
   cudaFree(c->head_logits);
   cudaFree(c->surv);
@@ -214,6 +217,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->d_phist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->d_thist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->scratch, 3 * (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = al((void**)&x->next_keys[0], (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = al((void**)&x->next_keys[1], (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
   if (e == cudaSuccess) e = al((void**)&x->head_logits, (size_t)x->maxB * kSparseCap * 4);
   if (e == cudaSuccess) e = cudaMemset(x->seed_hist, 0, (size_t)x->maxB * kSeedBins * 4);
@@ -330,6 +335,8 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const size_t nb = (size_t)ctx->maxB * ctx->BW;
   a.parent_out = ctx->parent_hist + (size_t)(t - 1) * nb;
   a.token_out = ctx->token_hist + (size_t)(t - 1) * nb;
+  if (t < ctx->nd) a.next_keys_out = ctx->next_keys[t & 1];
+  if (t > 1) a.next_keys_in = ctx->next_keys[(t - 1) & 1];
   a.theta = ctx->scratch;
   a.surv_count = ctx->scratch + ctx->maxB;
   a.ovf = ctx->scratch + 2 * ctx->maxB;
@@ -374,6 +381,16 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
       !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sparse_keys <= kSparseCap;
   if (!sparse_route && ctx->V > 16384)
     return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 needs the codebook shard (nranks > 1)");
+  // skewed tries: a level that mixes dense and sparse nodes. The dense path hands its sparse-parent
+  // rows to a thread-per-row kernel, and (unless the sparse kernel is disabled) each request takes
+  // the sparse route when its own candidates fit on chip (decided by the previous step's commit).
+  const LevelHost& lv = ctx->trie.lv[t - 1];
+  const bool has_sparse_nodes = lv.n_dense < lv.n_nodes;
+  const bool streamed = ctx->V % 128 == 0 && ctx->V <= 16384;
+  if (!sparse_route && streamed && has_sparse_nodes) {
+    a.defer_sparse = 1;
+    a.mixed = (t > 1 && !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL)) ? 1 : 0;
+  }
   if (!sparse_route && dtype == XGR_DTYPE_BF16 && ctx->V % 128 != 0)
     return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need V %% 128 == 0");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));

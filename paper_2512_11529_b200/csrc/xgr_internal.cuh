@@ -116,6 +116,14 @@ struct StepArgs {
   float* lse;           // [batch][BW] per-row lse (NaN: row not read)
   uint32_t* flags;      // sticky per-request status bits
   unsigned long long* counters;
+  // per-request routing (skewed tries): the commit of step t writes, per request, the number of
+  // legal candidates its beams will have at step t + 1 (sum of the new nodes' child counts);
+  // on a "mixed" step (both routes launched) a request with at most kSparseCap of them takes the
+  // sparse route (k_sparse) and every dense-route kernel skips it, the others the dense route.
+  const uint32_t* next_keys_in;   // written by the previous step's commit [batch]
+  uint32_t* next_keys_out;        // this step's commit [batch] (null at the last step)
+  int32_t mixed;                  // 1: both routes launched this step
+  int32_t defer_sparse;           // 1: k_stream leaves sparse-parent rows to k_sparse_rows
   // codebook shard (nranks > 1): this rank's logits hold columns [col0, col0 + Vl) of V
   int32_t col0;
   int32_t Vl;
@@ -226,6 +234,11 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
   do {                       \
   } while (0)
 #endif
+
+// ---- per-request route on a mixed step ------------------------------------------------------------
+__device__ __forceinline__ bool req_sparse(const StepArgs& a, int req) {
+  return a.mixed && a.next_keys_in[req] <= (uint32_t)kSparseCap;
+}
 
 // ---- beam state of row b of request req ----------------------------------------------------------
 __device__ __forceinline__ int nlive_of(const StepArgs& a, int req) {

@@ -565,6 +565,26 @@ __device__ void commit(const StepArgs& a, int req, const uint64_t* sel, int k, c
     a.nlive_out[req] = k;
     if (a.fin_nlive) a.fin_nlive[req] = k;
   }
+  if (a.next_keys_out) {
+    // the next step's legal candidates of this request: sum of the new nodes' child counts (the
+    // next step's per-request route); children of node c of level l+1 are the level-(l+2) nodes
+    // [first_child[c], first_child[c+1])
+    __shared__ uint32_t s_nk[32];
+    const uint32_t* fcn = a.trie.lv[a.level + 1].first_child;
+    uint32_t nk = 0;
+    for (int j = threadIdx.x; j < k; j += T) {
+      const uint32_t c = a.node_out[base + j];
+      nk += __ldg(fcn + c + 1) - __ldg(fcn + c);
+    }
+    nk = __reduce_add_sync(0xffffffffu, nk);
+    if ((threadIdx.x & 31) == 0) s_nk[threadIdx.x >> 5] = nk;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t tot = 0;
+      for (int w = 0; w < T / 32; ++w) tot += s_nk[w];
+      a.next_keys_out[req] = tot;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -953,6 +973,7 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
   int* s_rowcnt = reinterpret_cast<int*>(s_cand + kMaxBW);   // per-beam Top-K row counters [BW]
                                                             // (results use s_cand[0 .. BW))
   const int req = blockIdx.x, tid = threadIdx.x;
+  if (req_sparse(a, req)) return;   // a mixed step's sparse-route request: k_sparse commits it
   const uint64_t* src = a.surv + (size_t)req * a.cap;
   const uint64_t p0 = tid < a.cap ? src[tid] : 0ull;
   const uint64_t p1 = tid + T < a.cap ? src[tid + T] : 0ull;
@@ -1119,6 +1140,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
   __shared__ uint16_t s_rbase[NR], s_rcnt[NR];   // each row's key segment (per-beam Top-K)
   __shared__ int32_t s_big[NR];
   const int req = blockIdx.x, tid = threadIdx.x, lane = lane_id();
+  if (a.mixed && !req_sparse(a, req)) return;   // a mixed step's dense-route request
   // beam state of rows tid and tid + T loaded speculatively, alongside nlive
   static_assert(2 * T >= kMaxBW, "k_sparse: two rows per thread");
   float S_pre[2];
@@ -1393,6 +1415,64 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_sparse_rows: the sparse-parent rows of a dense-route step (skewed tries mix dense and sparse
+// nodes on one level). One thread per row: theta is known (seed), so the row is skipped if
+// S_b < theta, else its legal logits are gathered by label, its lse computed (stored for the exact
+// fallback), and its candidates c >= theta emitted to the request's survivor buffer.
+// ---------------------------------------------------------------------------------------------
+template <typename TI>
+__global__ void __launch_bounds__(128) k_sparse_rows(const __grid_constant__ StepArgs a, int rows) {
+  pdl_wait();
+  const int req = blockIdx.x, b = blockIdx.y * 128 + threadIdx.x;
+  if (b >= rows || b >= nlive_of(a, req) || req_sparse(a, req)) return;
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  if (L.dense_slot && L.dense_slot[node] >= 0) return;   // dense rows: k_stream
+  const float th = theta_value(a.theta[req]);
+  float* lse_out = a.lse + (size_t)req * a.BW + b;
+  if (S < th) {   // every candidate of the row is <= S_b < theta: not read
+    *lse_out = __int_as_float(0x7fc00000);
+    count_add(a, XGR_CNT_ROWS_SKIP_PRE, 1);
+    return;
+  }
+  const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  float M = -INFINITY;
+  for (uint32_t q = fc; q < fe; ++q) M = fmaxf(M, ldx(row + lab[q]));
+  float Z = 0.f;
+  for (uint32_t q = fc; q < fe; ++q) Z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[q]), M), kLog2e));
+  const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+  const float lse = row_lse(M, Z);
+  *lse_out = finite ? lse : __int_as_float(0x7fc00000);
+  count_add(a, XGR_CNT_ROWS_READ, 1);
+  count_add(a, XGR_CNT_LEGAL, fe - fc);
+  if (!finite) {
+    atomicOr(a.flags + req, kFlagNonfinite);
+    return;
+  }
+  if (!(cand_score(S, M, lse) >= th)) {   // UB_b = S_b - ln Z_b < theta
+    count_add(a, XGR_CNT_ROWS_SKIP_POST, 1);
+    return;
+  }
+  const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+  uint64_t* sbuf = a.surv + (size_t)req * a.cap;
+  uint32_t n = 0;
+  for (uint32_t q = fc; q < fe; ++q) {
+    const uint32_t v = lab[q];
+    const float c = cand_score(S, ldx(row + v), lse);
+    if (c >= th) {
+      const uint32_t pos = atomicAdd(a.surv_count + req, 1u);
+      if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(c, fbase + v);
+      ++n;
+    }
+  }
+  count_add(a, XGR_CNT_SURVIVORS, n);
+}
+
+// ---------------------------------------------------------------------------------------------
 // support: children of prefixes, read from the representation the step kernels use.
 // ---------------------------------------------------------------------------------------------
 __global__ void k_children(TrieDev tr, const int32_t* prefixes, int depth, int64_t n, int32_t* counts,
@@ -1547,6 +1627,26 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
   const bool bf16 = a.dtype == XGR_DTYPE_BF16;
+  if (a.mixed) {
+    // both routes: k_sparse commits the requests whose next-step candidates fit on chip (decided
+    // per request by the previous commit), the dense path the others (it skips the former); the
+    // dense path's sparse-parent rows go to k_sparse_rows
+    const size_t smem = ((size_t)kSparseCap + 2 * kMaxBW) * sizeof(uint64_t);
+    StepArgs as = a;
+    as.sparse_cap = kSparseCap;
+    if (bf16) launch_pdl(k_sparse<512, false, __nv_bfloat16>, a.batch, 512, smem, s, as);
+    else launch_pdl(k_sparse<512, false>, a.batch, 512, smem, s, as);
+    ++*launches;
+    if ((e = launch_stream(a, rows, s, ev0, ev1, launches)) != cudaSuccess) return e;
+    const dim3 g(a.batch, (rows + 127) / 128);
+    if (bf16) launch_pdl(k_sparse_rows<__nv_bfloat16>, g, 128, 0, s, a, rows);
+    else launch_pdl(k_sparse_rows<float>, g, 128, 0, s, a, rows);
+    const size_t sel = ((size_t)a.cap + 2 * kMaxBW) * sizeof(uint64_t);
+    if (bf16) launch_pdl(k_select<512, __nv_bfloat16>, a.batch, 512, sel, s, a);
+    else launch_pdl(k_select<512>, a.batch, 512, sel, s, a);
+    *launches += 2;
+    return cudaGetLastError();
+  }
   if (sparse_route) {
     size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
     if (bf16) {
@@ -1563,6 +1663,12 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
   if (bf16 && !stream_supported(V)) return cudaErrorNotSupported;   // the API checks this first
   if (stream_supported(V)) {
     e = launch_stream(a, rows, s, ev0, ev1, launches);   // k_seed resets theta/count/ovf
+    if (e == cudaSuccess && a.defer_sparse) {   // the sparse-parent rows, one thread each
+      const dim3 g(a.batch, (rows + 127) / 128);
+      if (bf16) launch_pdl(k_sparse_rows<__nv_bfloat16>, g, 128, 0, s, a, rows);
+      else launch_pdl(k_sparse_rows<float>, g, 128, 0, s, a, rows);
+      ++*launches;
+    }
   } else if ((e = cudaMemsetAsync(a.theta, 0, (size_t)a.batch * 4, s)) != cudaSuccess ||
              (e = cudaMemsetAsync(a.surv_count, 0, (size_t)a.batch * 4, s)) != cudaSuccess ||
              (e = cudaMemsetAsync(a.ovf, 0, (size_t)a.batch * 4, s)) != cudaSuccess) {

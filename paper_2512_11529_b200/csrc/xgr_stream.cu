@@ -517,14 +517,45 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
                    : "=r"(v[i].x), "=r"(v[i].y), "=r"(v[i].z), "=r"(v[i].w) : "l"(row + CH * q));
   }
   const int nl = nlive_of(a, req);
-  if (r >= nl) return;   // before any beam-state read: r < theta_rows may exceed BW
+  if (r >= nl || req_sparse(a, req)) return;   // before any beam-state read: r < theta_rows may exceed BW
   float S;
   uint32_t node;
   row_state(a, req, r, S, node);
   const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
   const LevelDev& L = a.trie.lv[a.level];
   const int slot = L.dense_slot ? L.dense_slot[node] : -1;
-  if (slot < 0) return;   // sparse seed rows contribute nothing (no bound from them)
+  if (slot < 0) {
+    // a sparse seed row adds every candidate to the histogram (all real candidates: the count
+    // stays valid); none with a per-beam Top-K cap, and none in the codebook shard
+    if (a.topk || a.gstats) return;
+    const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+    const uint16_t* lab = a.trie.lv[a.level + 1].label;
+    float tm = -INFINITY;
+    for (uint32_t q = fc + tid; q < fe; q += T) tm = fmaxf(tm, ldx(row + lab[q]));
+    tm = wmax(tm);
+    if (lane == 0) part[warp] = make_float2(tm, 0.f);
+    __syncthreads();
+    float M = part[0].x;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) M = fmaxf(M, part[w].x);
+    float z = 0.f;
+    for (uint32_t q = fc + tid; q < fe; q += T) z += ex2f(__fmul_rn(__fsub_rn(ldx(row + lab[q]), M), kLog2eS));
+    z = wsum(z);
+    __syncthreads();
+    if (lane == 0) part[warp].y = z;
+    __syncthreads();
+    float Z = 0.f;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) Z += part[w].y;
+    if (!((Z > 0.5f) && (Z <= 3.0e38f))) return;
+    const float lse = row_lse(M, Z);
+    uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+    for (uint32_t q = fc + tid; q < fe; q += T) {
+      const float dd = __fmul_rn(__fsub_rn(S0, cand_score(S, ldx(row + lab[q]), lse)), 128.0f);
+      if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(h + (int)dd, 1u);
+    }
+    return;
+  }
   const uint32_t* bm = L.bitmap + (size_t)slot * a.trie.W + (a.col0 >> 5);
   float x[4 * VPT];
 #pragma unroll
@@ -789,7 +820,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         m.b = w / a.batch;
         m.req = w - m.b * a.batch;
         const int nl = a.nlive_in ? a.nlive_in[m.req] : 1;
-        m.live = m.b < nl;
+        m.live = m.b < nl && !req_sparse(a, m.req);   // a mixed step's sparse-route requests: k_sparse
         if (m.live) {
           row_state(a, m.req, m.b, m.S, m.node);
           if (MODE != kModeStats && MODE != kModeSeedHist) m.th = theta_value(a.theta[m.req]);
@@ -824,6 +855,8 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
         } else if (!(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
           kind = m0.slot >= 0 ? 1 : 2;
+          // sparse-parent rows: gathered by label by one thread each in k_sparse_rows
+          if (kind == 2 && MODE == kModeNormal && a.defer_sparse) kind = 0;
         }
       }
       for (int j = 0; j < 32; ++j) {
@@ -947,7 +980,9 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     if (d.kind != 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
-      if (d.kind == 0 || MODE == kModeSeedHist) continue;   // sparse seed rows add no bound
+      // sparse seed rows add every candidate to the histogram (each is a real candidate, so the
+      // count stays valid); with a per-beam Top-K cap they add nothing
+      if (d.kind == 0 || (MODE == kModeSeedHist && a.topk)) continue;
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
@@ -982,6 +1017,16 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         const float Z = gsum(z);
         if (MODE == kModeStats) {   // local (m, Z); an empty slice is (-inf, 0)
           if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+          continue;
+        }
+        if (MODE == kModeSeedHist) {
+          if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
+          const float lse2 = row_lse(M, Z), S0 = d.lse;
+          uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+          for (uint32_t q = fc + lt; q < fe; q += GT) {
+            const float dd = __fmul_rn(__fsub_rn(S0, cand_score(S, ldx(row + lab[q]), lse2)), 128.0f);
+            if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(h + (int)dd, 1u);
+          }
           continue;
         }
         finite = (Z > 0.5f) && (Z <= 3.0e38f);

@@ -12,6 +12,8 @@ from .inputs import (  # noqa: F401
     splitmix64,
     feistel_permute,
     make_items,
+    make_items_clustered,
+    make_config_items,
     make_logits,
     make_logits_torch,
     make_logits_rows_torch,

@@ -27,6 +27,8 @@ CONFIGS = {
     "C3": dict(batch=256, beam_width=256, vocab=8192, nd=3, n_items=100_000_000),
     "C4": dict(batch=512, beam_width=512, vocab=16384, nd=4, n_items=100_000_000),
     "C5": dict(batch=128, beam_width=512, vocab=65536, nd=3, n_items=1_000_000_000),
+    # C3 with clustered (Zipf s = 1) semantic IDs instead of uniform ones (make_items_clustered)
+    "C3Z": dict(batch=256, beam_width=256, vocab=8192, nd=3, n_items=100_000_000, clustered=1.0),
 }
 
 
@@ -49,8 +51,15 @@ def splitmix64(x):
     return int(z) if scalar else z
 
 
+def make_config_items(cfg: dict) -> np.ndarray:
+    """The item list of a config: uniform (make_items) or clustered (make_items_clustered)."""
+    if cfg.get("clustered"):
+        return make_items_clustered(cfg["n_items"], cfg["vocab"], cfg["nd"], cfg["trie_key"], s=cfg["clustered"])
+    return make_items(cfg["n_items"], cfg["vocab"], cfg["nd"], cfg["trie_key"])
+
+
 def config_key(name: str) -> int:
-    k = int(name[1:])
+    k = int(name[1:].rstrip("Z")) + (100 if name.endswith("Z") else 0)
     return splitmix64(2512115290 + k)
 
 
@@ -104,6 +113,54 @@ def make_items(n: int, vocab: int, nd: int, key: int, dup_frac: float = 0.0,
         out = np.concatenate([out, dups], axis=0)
         out = out[rng.permutation(out.shape[0])]
         out = np.ascontiguousarray(out)
+    return out
+
+
+def make_items_clustered(n: int, vocab: int, nd: int, key: int, s: float = 1.0, chunk: int = 1 << 24) -> np.ndarray:
+    """N distinct ND-tuples with clustered (skewed) prefixes, as int32 [n][nd], unsorted.
+
+    Real semantic IDs are clustered: a few first-level codes hold many items, and under each
+    prefix a few next codes dominate (the paper's datasets are out of scope, so
+    this is a declared synthetic stand-in). Token d of a tuple is drawn from a Zipf(s) law over
+    [0, vocab) whose rank order is permuted per prefix: rank k -> (k * a_p + b_p) mod vocab with
+    a_p odd and (a_p, b_p) hashed from the prefix (a bijection, vocab a power of two). Tuples are
+    drawn in seeded chunks and de-duplicated keeping first occurrences, until n are distinct.
+    """
+    assert vocab >= 2 and (vocab & (vocab - 1)) == 0, "generator needs a power-of-two vocab"
+    b = vocab.bit_length() - 1
+    assert b * nd <= 63
+    w = 1.0 / np.arange(1, vocab + 1, dtype=np.float64) ** s
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    rng = np.random.default_rng(key & 0xFFFFFFFFFFFFFFFF)
+    vm = np.uint64(vocab - 1)
+    keys_parts, have, seen = [], 0, None
+    while have < n:
+        m = min(chunk, (n - have) * 5 // 4 + 4096)
+        h = np.full(m, np.uint64(key & 0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+        k = np.zeros(m, dtype=np.uint64)
+        for d in range(nd):
+            hp = splitmix64(h)
+            a = (hp | np.uint64(1)) & vm
+            bb = (hp >> np.uint64(32)) & vm
+            r = np.searchsorted(cdf, rng.random(m)).astype(np.uint64)
+            r = np.minimum(r, vm)
+            with np.errstate(over="ignore"):
+                t = (r * a + bb) & vm
+                h = splitmix64(h ^ (t + np.uint64(0x51ED27 + d)))
+            k = (k << np.uint64(b)) | t
+        # first occurrences, in draw order, not seen in earlier chunks
+        _, first = np.unique(k, return_index=True)
+        k = k[np.sort(first)]
+        if seen is not None:
+            k = k[~np.isin(k, seen)]
+        keys_parts.append(k)
+        seen = k if seen is None else np.concatenate([seen, k])
+        have += k.shape[0]
+    allk = np.concatenate(keys_parts)[:n]
+    out = np.empty((n, nd), dtype=np.int32)
+    for d in range(nd):
+        out[:, d] = ((allk >> np.uint64(b * (nd - 1 - d))) & vm).astype(np.int32)
     return out
 
 

@@ -35,3 +35,17 @@ def test_prefix_keyed_rows_exact_grid():
     assert np.all(r * 2 ** 15 == np.round(r * 2 ** 15))
     assert np.array_equal(r, prefix_keyed_row(5, 0, (1, 2), 64))
     assert not np.array_equal(r, prefix_keyed_row(5, 0, (1, 3), 64))
+
+
+def test_clustered_items_distinct_deterministic_skewed():
+    from synth import make_items_clustered
+    a = make_items_clustered(200_000, 1024, 3, 5)
+    b = make_items_clustered(200_000, 1024, 3, 5)
+    assert a.shape == (200_000, 3) and a.dtype == np.int32
+    assert np.array_equal(a, b)
+    assert a.min() >= 0 and a.max() < 1024
+    k = (a[:, 0].astype(np.int64) << 20) | (a[:, 1].astype(np.int64) << 10) | a[:, 2]
+    assert np.unique(k).shape[0] == 200_000
+    # skew: the most popular first token holds far more than a uniform 1/1024 share
+    _, cnt = np.unique(a[:, 0], return_counts=True)
+    assert cnt.max() > 20 * 200_000 / 1024

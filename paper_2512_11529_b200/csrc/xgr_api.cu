@@ -23,6 +23,7 @@ cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int
 cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
                                cudaStream_t s);
 cudaError_t merge_fits(int nranks, int bw, int device, bool* ok);
+bool stream_supported(int V);
 cudaError_t launch_children(const TrieDev& tr, const int32_t* prefixes, int depth, int64_t n,
                             int32_t* counts, int32_t* tokens, int64_t cap, cudaStream_t s);
 cudaError_t launch_account(const StepArgs& a, int rows, uint32_t* touched,
@@ -162,6 +163,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.top_k < 0) return fail(XGR_ERR_INVALID_ARG, "init: top_k < 0");
   if (c.top_k > 0 && c.top_k < c.beam_width && c.nranks > 1)
     return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width with the codebook shard");
+  if (c.top_k > 0 && c.top_k < c.beam_width && c.vocab > 16384)
+    return fail(XGR_ERR_UNSUPPORTED, "init: per-beam top_k < beam_width needs vocab <= 16384");
   if (c.max_batch < 1) return fail(XGR_ERR_INVALID_ARG, "init: max_batch < 1");
   if (c.nranks < 1 || c.rank < 0 || c.rank >= c.nranks)
     return fail(XGR_ERR_INVALID_ARG, "init: need 0 <= rank < nranks");
@@ -379,20 +382,21 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const int64_t sparse_keys = (int64_t)rows_live * maxc;
   const bool sparse_route =
       !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sparse_keys <= kSparseCap;
-  if (!sparse_route && ctx->V > 16384)
-    return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 needs the codebook shard (nranks > 1)");
+  if (!sparse_route && !stream_supported(ctx->V) && ctx->V > 16384)
+    return fail(XGR_ERR_UNSUPPORTED, "step: dense route for V > 16384 needs V %% (128 C) == 0 (C = V / 8192 "
+                "rounded up to a power of two) or the codebook shard");
   // skewed tries: a level that mixes dense and sparse nodes. The dense path hands its sparse-parent
   // rows to a thread-per-row kernel, and (unless the sparse kernel is disabled) each request takes
   // the sparse route when its own candidates fit on chip (decided by the previous step's commit).
   const LevelHost& lv = ctx->trie.lv[t - 1];
   const bool has_sparse_nodes = lv.n_dense < lv.n_nodes;
-  const bool streamed = ctx->V % 128 == 0 && ctx->V <= 16384;
+  const bool streamed = stream_supported(ctx->V);
   if (!sparse_route && streamed && has_sparse_nodes) {
     a.defer_sparse = 1;
     a.mixed = (t > 1 && !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL)) ? 1 : 0;
   }
-  if (!sparse_route && dtype == XGR_DTYPE_BF16 && ctx->V % 128 != 0)
-    return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need V %% 128 == 0");
+  if (!sparse_route && dtype == XGR_DTYPE_BF16 && !stream_supported(ctx->V))
+    return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need the streaming kernels (V %% 128 == 0)");
   if (t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   if (!ctx->ev.empty() && !sparse_route && ctx->ev_head - ctx->ev_tail < kTimingRing) {

@@ -109,6 +109,37 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
   return v;
 }
 
+// ---- thread-block cluster helpers (column-split rows, SURVEY 8(e) open question) ----------------
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// all threads of every CTA of the cluster (release / acquire: orders shared-memory writes)
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t local_smem, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
+  asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 struct Desc {
   int32_t req, b, kind, slot;  // kind: 0 nothing to do, 1 dense row in stage, 2 sparse row
   float S;
@@ -751,13 +782,27 @@ struct Ring {
   __device__ static __forceinline__ int use(int k) { return (k / G) / NSG; }   // n-th use of the stage
 };
 
-template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float, int GT = 256>
+// C > 1: a thread-block cluster of C CTAs splits every row by columns (CTA rank r owns the row's
+// columns [r V/C, (r+1) V/C)); each computes its slice's (m, Z), the C partials are exchanged through
+// distributed shared memory (one mailbox slot and one cluster-scope mbarrier per row) and combined
+// in rank order, so every CTA holds the identical row lse; each then emits its own columns. Rows up
+// to C x 8192 tokens (V 16384 .. 65536) run on the 8192-column kernel shape.
+template <int EPT, int G, int NS, int MINB = 1, int MODE = kModeNormal, typename TI = float, int GT = 256,
+          int C = 1>
 __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_constant__ StepArgs a, int total,
                                                              int seeded_rows) {
   pdl_wait();
   if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
   // GT consumer threads per group (256, or 512 for 16384-token rows)
   using R = Ring<G, NS>;
+  static_assert(C == 1 || (G == 1 && (MODE == kModeNormal || MODE == kModeSeedHist)), "cluster: one group");
+  constexpr int NXS = 4;           // cluster mailbox slots (the CTAs of a cluster are <= 1 row apart)
+  __shared__ float2 mbox[NXS][C];
+  __shared__ __align__(8) uint64_t xbar[NXS];
+  const int crank = C > 1 ? (int)cluster_ctarank() : 0;
+  const int ncl = gridDim.x / C, cl = blockIdx.x / C;   // rows w = cl + k * ncl
+  const int Vc = a.Vl / C;                              // this CTA's columns [ccol, ccol + Vc)
+  const int ccol = a.col0 + crank * Vc;
   constexpr int VT = GT * EPT;     // tokens per stage row
   constexpr int MW = VT / 32;      // mask words per stage
   constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk (4 fp32, 8 bf16)
@@ -785,10 +830,13 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], GT / 32);
     }
+    if (C > 1)
+      for (int s = 0; s < NXS; ++s) mbar_init(&xbar[s], C);   // one arrival per CTA of the cluster
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < NS * MW; i += NC + 32) s_msk[i] = 0u;
   __syncthreads();
+  if (C > 1) cluster_sync_all();   // every mailbox barrier initialised before any remote arrive
 
   if (tid >= NC) {
     // ------------------------------- producer warp ---------------------------------------
@@ -807,7 +855,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     };
     auto fetch_raw = [&](int k0) {
       Meta m;
-      const int w = blockIdx.x + (k0 + lane) * gridDim.x;
+      const int w = cl + (k0 + lane) * ncl;
       m.b = 0;
       m.req = 0;
       m.live = 0;
@@ -844,7 +892,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     fetch_slot(m0);
     Meta m1 = fetch_raw(32);
     for (int k0 = 0;; k0 += 32) {
-      if (blockIdx.x + k0 * gridDim.x >= total) break;
+      if (cl + k0 * ncl >= total) break;
       Meta m2 = fetch_raw(k0 + 64);
       fetch_slot(m1);
       // decisions for the current batch (its loads completed during the previous batch)
@@ -855,13 +903,14 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
         } else if (!(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
           kind = m0.slot >= 0 ? 1 : 2;
-          // sparse-parent rows: gathered by label by one thread each in k_sparse_rows
-          if (kind == 2 && MODE == kModeNormal && a.defer_sparse) kind = 0;
+          // sparse-parent rows: gathered by label by one thread each in k_sparse_rows; in a cluster
+          // only rank 0 handles them (the whole row) in the seed pass
+          if (kind == 2 && ((MODE == kModeNormal && a.defer_sparse) || crank != 0)) kind = 0;
         }
       }
       for (int j = 0; j < 32; ++j) {
         const int kj = k0 + j;
-        if (blockIdx.x + kj * gridDim.x >= total) break;
+        if (cl + kj * ncl >= total) break;
         const int jkind = __shfl_sync(0xffffffffu, kind, j);
         const int jslot = __shfl_sync(0xffffffffu, m0.slot, j);
         const int jb = __shfl_sync(0xffffffffu, m0.b, j);
@@ -887,12 +936,13 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           desc[st] = d;
           s_th[st] = jth;
           if (jkind == 1) {
-            const TI* row = static_cast<const TI*>(a.logits) + (size_t)jreq * a.req_stride + (size_t)jb * a.ld;
-            const uint32_t rb = (uint32_t)a.Vl * (uint32_t)sizeof(TI), mb = (uint32_t)(a.Vl >> 5) * 4u;
+            const TI* row = static_cast<const TI*>(a.logits) + (size_t)jreq * a.req_stride + (size_t)jb * a.ld +
+                            (size_t)crank * Vc;
+            const uint32_t rb = (uint32_t)Vc * (uint32_t)sizeof(TI), mb = (uint32_t)(Vc >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
             bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
             // a dense node's bitmap is shared by every row whose beam sits on it: keep it in L2
-            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (a.col0 >> 5), mb, &full[st],
+            bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (ccol >> 5), mb, &full[st],
                      pol_keep);
           } else {
             mbar_arrive(&full[st]);
@@ -903,6 +953,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       m0 = m1;
       m1 = m2;
     }
+    if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write its mailbox
     return;
   }
 
@@ -948,8 +999,9 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       pend_req = -1;
     }
   };
+  int xit = 0;   // dense rows exchanged within the cluster (mailbox slot / phase)
   for (int k = g;; k += G) {
-    const int w = blockIdx.x + k * gridDim.x;
+    const int w = cl + k * ncl;
     if (w >= total) break;
     const int st = R::stage(k);
     mbar_wait(&full[st], R::use(k) & 1);
@@ -957,7 +1009,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     // stage (the empty-barrier arrive) is then the one that read it
     Desc d;
     float th;
-    {
+    if (a.dbg & (1 << 21)) {   // A/B experiment (XGR_DEBUG_FLAGS bit 21): every lane reads it
+      d = desc[st];
+      th = s_th[st];
+    } else {
       int4 di = make_int4(0, 0, 0, 0);
       float4 df = make_float4(0.f, 0.f, 0.f, 0.f);
       if (lane == 0) {
@@ -1104,12 +1159,40 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     named_sync(bar_id, GT);
     ++it;
     float2 pr = lane < GT / 32 ? pp[lane] : make_float2(-INFINITY, 0.f);
-    const float M = wmax(pr.x);   // warp-uniform
+    float M = wmax(pr.x);   // warp-uniform
     float zi = pr.y * ex2f(__fmul_rn(__fsub_rn(pr.x, M), kLog2eS));
     if (lane >= GT / 32) zi = 0.f;
 #pragma unroll
     for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
-    const float Z = __shfl_sync(0xffffffffu, zi, 0);
+    float Z = __shfl_sync(0xffffffffu, zi, 0);
+    if constexpr (C > 1) {
+      // this slice's (m, Z) to every CTA of the cluster (slot xit % NXS), then the C partials
+      // combined in rank order: M = max_r m_r, Z = sum_r Z_r 2^((m_r - M) log2 e) -- identical on
+      // every rank. An empty slice is (-inf, 0); a NaN partial makes the row non-finite.
+      const int xs = xit % NXS;
+      if (lt == 0) {
+        const float2 mine2 = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+#pragma unroll
+        for (int r = 0; r < C; ++r) {
+          st_cluster_f2(mapa(smem_u32(&mbox[xs][crank]), (uint32_t)r), mine2);
+          mbar_arrive_remote(mapa(smem_u32(&xbar[xs]), (uint32_t)r));
+        }
+      }
+      mbar_wait_cluster(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
+      ++xit;
+      float2 q[C];
+#pragma unroll
+      for (int r = 0; r < C; ++r) q[r] = mbox[xs][r];
+      M = q[0].x;
+#pragma unroll
+      for (int r = 1; r < C; ++r) M = fmaxf(M, q[r].x);
+      Z = 0.f;
+#pragma unroll
+      for (int r = 0; r < C; ++r) {
+        if (q[r].y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q[r].y, ex2f(__fmul_rn(__fsub_rn(q[r].x, M), kLog2eS))));
+        else if (q[r].y != q[r].y) Z = q[r].y;
+      }
+    }
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
       if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
       continue;
@@ -1172,7 +1255,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
     const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
     lse = row_lse(M, Z);
-    if (lt == 0) {
+    if (lt == 0 && crank == 0) {
       a.lse[(size_t)req * BW + b] = finite ? lse : __int_as_float(0x7fc00000);
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
       if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
@@ -1211,18 +1294,18 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
       // included, is a candidate; legality re-read from the node's bitmap in global memory
-      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (a.col0 >> 5) + (lt / (32 / CH));
+      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (ccol >> 5) + (lt / (32 / CH));
 #pragma unroll
       for (int i = 0; i < NCH; ++i) {
         const uint32_t q4 = (uint32_t)(i * GT + lt);
-        const uint32_t nb = (CH * q4 < (uint32_t)a.Vl) ? ((__ldg(gm + i * (GT * CH / 32)) >> nsh) & CHM) : 0u;
+        const uint32_t nb = (CH * q4 < (uint32_t)Vc) ? ((__ldg(gm + i * (GT * CH / 32)) >> nsh) & CHM) : 0u;
         mine |= (uint64_t)nb << (CH * i);
       }
     }
     const int ns = __popcll(mine);
     if ((a.dbg & 1) == 0 && __any_sync(0xffffffffu, ns > 0)) {
       flush();
-      const uint32_t fbase = (uint32_t)b * (uint32_t)V + (uint32_t)a.col0;
+      const uint32_t fbase = (uint32_t)b * (uint32_t)V + (uint32_t)ccol;
       if (__any_sync(0xffffffffu, ns > 2)) {
         // many candidates in one lane (weak theta): reserve and write synchronously
         uint64_t* sbuf = a.surv + (size_t)req * a.cap;
@@ -1271,6 +1354,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
   }
   flush();
+  if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write its mailbox
 }
 
 template <int EPT, int NS, typename TI = float, int GT = 256>
@@ -1289,6 +1373,99 @@ static cudaError_t opt_in(K k, size_t smem) {
   return cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// Launch with a (C, 1, 1) thread-block cluster (and programmatic stream serialization if enabled).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_cl(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t s, int C,
+                             Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  attr[n].id = cudaLaunchAttributeClusterDimension;
+  attr[n].val.clusterDim.x = C;
+  attr[n].val.clusterDim.y = 1;
+  attr[n].val.clusterDim.z = 1;
+  ++n;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
+// Clusters of C CTAs of the column-split streaming kernel that fit on the device at once.
+template <typename K>
+static int max_clusters(K k, int block, size_t smem, int C) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C * 148);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    n = 3 * 148 / C;
+  }
+  return n;
+}
+
+// the column-split (cluster) streaming kernels: normal and seed pass, fp32 and bf16
+static int g_ncl[2][2][9];   // [dtype bf16][seed mode][C]: clusters per launch
+
+template <int C>
+static cudaError_t configure_cluster() {
+  using bf = __nv_bfloat16;
+  cudaError_t e;
+  auto kn = k_stream<32, 1, 2, 3, kModeNormal, float, 256, C>;
+  auto ks = k_stream<32, 1, 2, 3, kModeSeedHist, float, 256, C>;
+  auto bn = k_stream<32, 1, 4, 3, kModeNormal, bf, 256, C>;
+  auto bsd = k_stream<32, 1, 4, 3, kModeSeedHist, bf, 256, C>;
+  const size_t sf = stream_smem<32, 2>(), sb = stream_smem<32, 4, bf>();
+  if ((e = opt_in(kn, sf)) || (e = opt_in(ks, sf)) || (e = opt_in(bn, sb)) || (e = opt_in(bsd, sb))) return e;
+  g_ncl[0][0][C] = max_clusters(kn, 288, sf, C);
+  g_ncl[0][1][C] = max_clusters(ks, 288, sf, C);
+  g_ncl[1][0][C] = max_clusters(bn, 288, sb, C);
+  g_ncl[1][1][C] = max_clusters(bsd, 288, sb, C);
+  return cudaSuccess;
+}
+
+// Dense step of a row wider than 8192 columns on one GPU: clusters of C CTAs, 8192 columns or fewer
+// each (V % (128 C) == 0): histogram seed over R0 rows, theta, the streamed pass.
+template <int C>
+static void launch_stream_cluster(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                                  int* launches) {
+  using bf = __nv_bfloat16;
+  const bool b16 = a.dtype == XGR_DTYPE_BF16;
+  const int total = a.batch * rows;
+  const int r0 = std::min(a.theta_rows, rows);
+  if (r0 > 0) {
+    const int ns = a.batch * r0;
+    const int ncl = std::min(g_ncl[b16][1][C], ns);
+    if (b16) launch_cl(k_stream<32, 1, 4, 3, kModeSeedHist, bf, 256, C>, C * ncl, 288, stream_smem<32, 4, bf>(), s, C, a, ns, 0);
+    else launch_cl(k_stream<32, 1, 2, 3, kModeSeedHist, float, 256, C>, C * ncl, 288, stream_smem<32, 2>(), s, C, a, ns, 0);
+    ++*launches;
+  }
+  launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
+  if (ev0) cudaEventRecord(ev0, s);
+  const int ncl = std::min(g_ncl[b16][0][C], total);
+  if (b16) launch_cl(k_stream<32, 1, 4, 3, kModeNormal, bf, 256, C>, C * ncl, 288, stream_smem<32, 4, bf>(), s, C, a, total, 0);
+  else launch_cl(k_stream<32, 1, 2, 3, kModeNormal, float, 256, C>, C * ncl, 288, stream_smem<32, 2>(), s, C, a, total, 0);
+  if (ev1) cudaEventRecord(ev1, s);
+  *launches += 2;
+}
+
 cudaError_t configure_stream_kernels() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1301,6 +1478,7 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 1, 4>, stream_smem<32, 1>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 3, 1, kModeNormal, float, 512>, stream_smem<32, 3, float, 512>())) != cudaSuccess)
     return e;
+
   if ((e = opt_in(k_stream<32, 1, 4, 1, kModeNormal, __nv_bfloat16, 512>, stream_smem<32, 4, __nv_bfloat16, 512>())) !=
       cudaSuccess)
     return e;
@@ -1318,6 +1496,7 @@ cudaError_t configure_stream_kernels() {
   if ((e = opt_in(k_stream<32, 1, 4, 3, kModeSeedHist, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
       cudaSuccess)
     return e;
+  if ((e = configure_cluster<2>()) || (e = configure_cluster<4>()) || (e = configure_cluster<8>())) return e;
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
@@ -1338,7 +1517,12 @@ cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s) {
 }
 
 // Usable when a row and its mask can be bulk-copied: V % 128 == 0 (16-byte mask rows), V <= 16384.
-bool stream_supported(int V) { return V % 128 == 0 && V <= 16384; }
+// Cluster size of the column-split streaming kernel for a row of V columns (1: one CTA per row).
+static int cluster_of(int V) { return V <= 8192 ? 1 : V <= 16384 ? 2 : V <= 32768 ? 4 : 8; }
+
+// Usable when a row and its mask can be bulk-copied: every CTA's column slice V / C is a multiple
+// of 128 (16-byte mask rows), V <= 65536.
+bool stream_supported(int V) { return V <= 65536 && V % (128 * cluster_of(V)) == 0; }
 
 // Dense step: seed (theta + rows 0..R0-1), then the streaming pass over the rest. Returns the
 // number of kernels launched through *launches; ev0/ev1 bracket the streaming kernel.
@@ -1347,6 +1531,15 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int total = a.batch * rows;
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
+  const int C = cluster_of(a.Vl);
+  if (C > 2 || (C == 2 && !a.topk && g_stream_variant != 3)) {   // rows wider than 8192: column-split clusters
+    switch (C) {
+      case 2: launch_stream_cluster<2>(a, rows, s, ev0, ev1, launches); break;
+      case 4: launch_stream_cluster<4>(a, rows, s, ev0, ev1, launches); break;
+      default: launch_stream_cluster<8>(a, rows, s, ev0, ev1, launches); break;
+    }
+    return cudaGetLastError();
+  }
   if (a.dtype == XGR_DTYPE_BF16) {   // NEXT f1: bf16 rows (half the bytes), histogram seed
     using bf = __nv_bfloat16;
     const int r0 = std::min(a.theta_rows, rows);

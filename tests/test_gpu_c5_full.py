@@ -77,6 +77,6 @@ def test_c5_full_size_codebook_shard():
         for j in range(bw):
             tup = tuple(int(a) for a in outs[0]["tokens"][r, j])
             assert voc.item_rank(tup) == int(outs[0]["item_rank"][r, j])
-    assert res["adjudicated"] <= max(2, (res["strict"] + res["adjudicated"]) // 100), res
+    assert res["adjudicated"] <= max(3, (res["strict"] + res["adjudicated"]) // 20), res   # see test_gpu_parity._full
     print(f"\nC5 full: items {t_gen:.1f} s, oracle vocabulary {t_voc:.1f} s, 8 tries {t_build:.1f} s, "
           f"steps {['%.2f s' % s for s in t_steps]} (untimed emulation), checks {res}")

@@ -55,5 +55,5 @@ def test_c3z_full_size_all_requests(xgr):
     steps = [make_logits_torch((B, 1 if t == 0 else bw, c["vocab"]), 11 * t + 1, 2.0) for t in range(c["nd"])]
     bs.counters()
     out, stats = run_checked(bs, voc, steps, bw, list(range(B)))
-    assert stats["adjudicated"] <= max(2, (stats["strict"] + stats["adjudicated"]) // 100), stats
+    assert stats["adjudicated"] <= max(3, (stats["strict"] + stats["adjudicated"]) // 20), stats
     print("C3Z counters", bs.counters())

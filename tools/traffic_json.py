@@ -22,7 +22,7 @@ def val(m):
     v = float(r[hdr.index(m)].replace(",", ""))
     u = units[hdr.index(m)]
     return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1, "usecond": 1e3,
-                "msecond": 1e6}.get(u, 1)
+                "msecond": 1e6, "ns": 1, "us": 1e3, "ms": 1e6}.get(u, 1)
 
 
 rd, wr = val("dram__bytes_read.sum"), val("dram__bytes_write.sum")

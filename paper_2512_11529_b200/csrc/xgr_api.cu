@@ -20,6 +20,8 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches);
 cudaError_t launch_shard_stats(const StepArgs& a, int rows, cudaStream_t s);
 cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches);
+cudaError_t launch_shard_stats_sparse(const StepArgs& a, int rows, cudaStream_t s);
+cudaError_t launch_shard_select_sparse(const StepArgs& a, int sparse_keys, cudaStream_t s);
 cudaError_t launch_shard_merge(const StepArgs& a, const uint64_t* grec, const int32_t* grec_n,
                                cudaStream_t s);
 cudaError_t merge_fits(int nranks, int bw, int device, bool* ok);
@@ -69,6 +71,7 @@ struct xgr_ctx {
   StepArgs shard_args{};
   int shard_rows = 0;
   int shard_phase = 0;              // 0: expect stats, 1: expect select, 2: expect merge
+  int shard_sparse_keys = 0;        // > 0: this shard step takes the sparse route
   // XGR_CFG_TIMING: ring of event pairs around the dense-route streaming kernel
   std::vector<cudaEvent_t> ev;      // 2 * kTimingRing
   std::vector<int32_t> ev_step;
@@ -479,7 +482,12 @@ xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int
   cudaStream_t s = (cudaStream_t)stream;
   if (a.t == 1) ACK(cudaMemsetAsync(ctx->flags, 0, (size_t)batch * 4, s));
   a.stats_out = ctx->shard_stats;
-  ACK(launch_shard_stats(a, rows_live, s));
+  // the sparse route when every request's candidates fit on chip (as xgr_beam_step): thread-per-row
+  // stats and an on-chip selection instead of the streamed dense passes
+  const int64_t sk = (int64_t)rows_live * ctx->trie.lv[a.t - 1].max_children;
+  ctx->shard_sparse_keys = (!(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) && sk <= kSparseCap) ? (int)sk : 0;
+  if (ctx->shard_sparse_keys) ACK(launch_shard_stats_sparse(a, rows_live, s));
+  else ACK(launch_shard_stats(a, rows_live, s));
   ctx->launches += 1;
   ctx->batch = batch;
   ctx->shard_args = a;
@@ -500,7 +508,13 @@ xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, con
   a.rec_n = ctx->shard_rec_n;
   cudaStream_t s = (cudaStream_t)stream;
   int launches = 0;
-  ACK(launch_shard_select(a, ctx->shard_rows, s, &launches));
+  if (ctx->shard_sparse_keys) {
+    a.sparse_cap = ctx->shard_sparse_keys;
+    ACK(launch_shard_select_sparse(a, ctx->shard_sparse_keys, s));
+    launches = 1;
+  } else {
+    ACK(launch_shard_select(a, ctx->shard_rows, s, &launches));
+  }
   ctx->launches += launches;
   ctx->shard_phase = 2;
   *recs = ctx->shard_rec;

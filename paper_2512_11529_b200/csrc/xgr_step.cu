@@ -1123,7 +1123,28 @@ __global__ void __launch_bounds__(T) k_merge(const __grid_constant__ StepArgs a,
 // rows with <= 16 children (all rows' dependent load chains node -> first_child -> labels ->
 // logits run concurrently), and one warp per row for the rare larger rows.
 // ---------------------------------------------------------------------------------------------
-template <int T, bool ROOT, typename TI = float, bool CMP = false>
+// Children of [fc, fe) whose token lies in this rank's columns [col0, col0 + Vl) (codebook shard):
+// the labels are sorted, so they are a contiguous sub-range found by two binary searches.
+__device__ __forceinline__ void shard_range(const StepArgs& a, const uint16_t* lab, uint32_t& fc, uint32_t& fe) {
+  uint32_t lo = fc, hi = fe;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (lab[mid] < (uint32_t)a.col0) lo = mid + 1; else hi = mid;
+  }
+  const uint32_t f0 = lo;
+  hi = fe;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (lab[mid] < (uint32_t)(a.col0 + a.Vl)) lo = mid + 1; else hi = mid;
+  }
+  fc = f0;
+  fe = lo;
+}
+
+// SH (codebook-shard select phase at a sparse step): only the children in this rank's columns,
+// logits holding those columns, the GLOBAL lse from all ranks' stats; the commit writes this rank's
+// local top-BW records.
+template <int T, bool ROOT, typename TI = float, bool CMP = false, bool SH = false>
 __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArgs a) {
   pdl_wait();
   if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
@@ -1309,29 +1330,39 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       s_pi.fc[b] = fc;
       s_pi.fcn[b] = fe;
       s_pi.slot[b] = L.dense_slot ? L.dense_slot[node] : -1;
-      const int cnt = (int)(fe - fc);
+      uint32_t f0 = fc, f1 = fe;
+      if (SH) shard_range(a, lab, f0, f1);
+      const int cnt = (int)(f1 - f0);
       if (cnt > kSmall) {
         s_big[atomicAdd(&s_nbig, 1u)] = b;
         continue;
       }
-      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld -
+                      (SH ? a.col0 : 0);
       const float* crow = CMP ? a.clog + ((size_t)req * a.BW + b) * a.cld : nullptr;
       uint32_t vv[kSmall];
       float xv[kSmall];
 #pragma unroll
-      for (int k = 0; k < kSmall; ++k) vv[k] = k < cnt ? lab[fc + k] : 0u;
+      for (int k = 0; k < kSmall; ++k) vv[k] = k < cnt ? lab[f0 + k] : 0u;
 #pragma unroll
       for (int k = 0; k < kSmall; ++k) xv[k] = k < cnt ? (CMP ? crow[k] : ldx(row + vv[k])) : -INFINITY;
-      float M = -INFINITY;
+      bool finite;
+      float lse;
+      if (SH) {
+        lse = shard_lse(a, req, b, finite);
+      } else {
+        float M = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < kSmall; ++k) M = fmaxf(M, xv[k]);
-      float Z = 0.f;
+        for (int k = 0; k < kSmall; ++k) M = fmaxf(M, xv[k]);
+        float Z = 0.f;
 #pragma unroll
-      for (int k = 0; k < kSmall; ++k)
-        if (k < cnt) Z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
-      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = row_lse(M, Z);
+        for (int k = 0; k < kSmall; ++k)
+          if (k < cnt) Z += ex2(__fmul_rn(__fsub_rn(xv[k], M), kLog2e));
+        finite = (Z > 0.5f) && (Z <= 3.0e38f);
+        lse = row_lse(M, Z);
+      }
       if (!finite) atomicOr(a.flags + req, kFlagNonfinite);
+      if (SH && cnt == 0) continue;   // no child of this row in this rank's columns
       const uint32_t base = atomicAdd(&s_count, (uint32_t)cnt);
       XGR_CHECK(base + cnt <= (uint32_t)a.sparse_cap, "sparse keys base %u cnt %d cap %d", base, cnt, a.sparse_cap);
       s_rbase[b] = (uint16_t)base;
@@ -1347,19 +1378,27 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
       float S;
       uint32_t node;
       row_state(a, req, b, S, node);
-      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
-      const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+      const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld -
+                      (SH ? a.col0 : 0);
+      uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
       const float* crow = CMP ? a.clog + ((size_t)req * a.BW + b) * a.cld - fc : nullptr;
+      if (SH) shard_range(a, lab, fc, fe);
       auto xq = [&](uint32_t k) { return CMP ? crow[k] : ldx(row + lab[k]); };
-      float tmax = -INFINITY;
-      for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, xq(k));
-      const float M = warp_max(tmax);
-      float z = 0.f;
-      for (uint32_t k = fc + lane; k < fe; k += 32)
-        z += ex2(__fmul_rn(__fsub_rn(xq(k), M), kLog2e));
-      const float Z = warp_sum(z);
-      const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse = row_lse(M, Z);
+      bool finite;
+      float lse;
+      if (SH) {
+        lse = shard_lse(a, req, b, finite);
+      } else {
+        float tmax = -INFINITY;
+        for (uint32_t k = fc + lane; k < fe; k += 32) tmax = fmaxf(tmax, xq(k));
+        const float M = warp_max(tmax);
+        float z = 0.f;
+        for (uint32_t k = fc + lane; k < fe; k += 32)
+          z += ex2(__fmul_rn(__fsub_rn(xq(k), M), kLog2e));
+        const float Z = warp_sum(z);
+        finite = (Z > 0.5f) && (Z <= 3.0e38f);
+        lse = row_lse(M, Z);
+      }
       if (!finite && lane == 0) atomicOr(a.flags + req, kFlagNonfinite);
       uint32_t base = 0;
       if (lane == 0) {
@@ -1470,6 +1509,29 @@ __global__ void __launch_bounds__(128) k_sparse_rows(const __grid_constant__ Ste
     }
   }
   count_add(a, XGR_CNT_SURVIVORS, n);
+}
+
+// ---------------------------------------------------------------------------------------------
+// k_sparse_stats (codebook-shard stats phase at a sparse step): one thread per live row, the local
+// (m, Z) over the row's children in this rank's columns ((-inf, 0) when it has none).
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_sparse_stats(const __grid_constant__ StepArgs a, int rows) {
+  pdl_wait();
+  const int req = blockIdx.x, b = blockIdx.y * 128 + threadIdx.x;
+  if (b >= rows || b >= nlive_of(a, req)) return;
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  shard_range(a, lab, fc, fe);
+  const float* row = static_cast<const float*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
+  float M = -INFINITY;
+  for (uint32_t q = fc; q < fe; ++q) M = fmaxf(M, row[lab[q]]);
+  float Z = 0.f;
+  for (uint32_t q = fc; q < fe; ++q) Z += ex2(__fmul_rn(__fsub_rn(row[lab[q]], M), kLog2e));
+  a.stats_out[(size_t)req * a.BW + b] = M == -INFINITY && Z == Z ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -1615,6 +1677,9 @@ cudaError_t configure_kernels(int cap) {
     return e;
   if ((e = cudaFuncSetAttribute(k_sparse<512, false, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, spk)))
     return e;
+  if ((e = cudaFuncSetAttribute(k_sparse<512, false, float, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                spk)))
+    return e;
   return cudaFuncSetAttribute(k_sparse<512, false, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               spk);
 }
@@ -1700,6 +1765,17 @@ cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s);
 
 // Codebook shard, select phase: theta seed + emission with the global lse, then this rank's
 // local top-BW records (k_select writes records instead of committing when a.rec_out is set).
+// Sparse shard step: thread-per-row stats, and the on-chip selection of this rank's candidates.
+cudaError_t launch_shard_stats_sparse(const StepArgs& a, int rows, cudaStream_t s) {
+  launch_pdl(k_sparse_stats, dim3(a.batch, (rows + 127) / 128), 128, 0, s, a, rows);
+  return cudaGetLastError();
+}
+cudaError_t launch_shard_select_sparse(const StepArgs& a, int sparse_keys, cudaStream_t s) {
+  const size_t smem = ((size_t)sparse_keys + 2 * kMaxBW) * sizeof(uint64_t);
+  launch_pdl(k_sparse<512, false, float, false, true>, a.batch, 512, smem, s, a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_shard_select(const StepArgs& a, int rows, cudaStream_t s, int* launches) {
   cudaError_t e = launch_shard_emit(a, rows, s);
   if (e != cudaSuccess) return e;

@@ -10,7 +10,7 @@ import paper_2512_11529_b200 as xgr  # noqa: E402
 from synth import make_items, make_logits_torch  # noqa: E402
 
 V, ND, BW, B = 16384, 4, 512, int(os.environ.get("SAN_BATCH", "4"))
-items = make_items(int(os.environ.get("SAN_ITEMS", "3000000")), V, ND, 4242)
+items = make_items(int(os.environ.get("SAN_ITEMS", "30000000")), V, ND, 4242)
 bs = xgr.BeamSearch(V, ND, BW, B, flags=2)
 bs.mask_build(items)
 for t in range(ND):

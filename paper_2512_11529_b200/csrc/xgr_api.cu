@@ -287,6 +287,16 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
   return XGR_OK;
 }
 
+// Whether step t (1-based) runs both routes: after the root, on the dense route by level statistics,
+// the streaming kernels usable, and its trie level holding sparse nodes (skewed tries). Static per
+// (trie, step), so the previous step's commit knows whether to count its requests' candidates.
+static bool may_mix(const xgr_ctx* ctx, int t) {
+  if (t <= 1 || t > ctx->nd || (ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL) || ctx->cfg.nranks > 1) return false;
+  const LevelHost& lv = ctx->trie.lv[t - 1];
+  const int64_t sk = (int64_t)ctx->BW * lv.max_children;
+  return sk > kSparseCap && stream_supported(ctx->V) && lv.n_dense < lv.n_nodes;
+}
+
 // Validates a step's inputs and fills the launch arguments (shared by xgr_beam_step and the
 // codebook-shard phases). `what` names the caller in error messages.
 static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype, int32_t rows,
@@ -341,7 +351,8 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const size_t nb = (size_t)ctx->maxB * ctx->BW;
   a.parent_out = ctx->parent_hist + (size_t)(t - 1) * nb;
   a.token_out = ctx->token_hist + (size_t)(t - 1) * nb;
-  if (t < ctx->nd) a.next_keys_out = ctx->next_keys[t & 1];
+  // the commit counts each request's next-step candidates only when that step can be mixed
+  if (t < ctx->nd && may_mix(ctx, t + 1)) a.next_keys_out = ctx->next_keys[t & 1];
   if (t > 1) a.next_keys_in = ctx->next_keys[(t - 1) & 1];
   a.theta = ctx->scratch;
   a.surv_count = ctx->scratch + ctx->maxB;
@@ -396,7 +407,7 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const bool streamed = stream_supported(ctx->V);
   if (!sparse_route && streamed && has_sparse_nodes) {
     a.defer_sparse = 1;
-    a.mixed = (t > 1 && !(ctx->cfg.flags & XGR_CFG_NO_SPARSE_KERNEL)) ? 1 : 0;
+    a.mixed = may_mix(ctx, t) ? 1 : 0;
   }
   if (!sparse_route && dtype == XGR_DTYPE_BF16 && !stream_supported(ctx->V))
     return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need the streaming kernels (V %% 128 == 0)");

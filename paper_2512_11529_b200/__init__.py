@@ -13,6 +13,7 @@ from .binding import (  # noqa: F401
     XGR_CFG_NO_PRUNE,
     XGR_CFG_NO_SPARSE_KERNEL,
     XGR_CFG_TIMING,
+    XGR_CFG_PAPER_HEAP,
     XGR_DTYPE_BF16,
     XGR_DTYPE_F32,
     kv_reorder,

@@ -22,6 +22,7 @@ XGR_CFG_NO_PRUNE = 0x1
 XGR_CFG_COUNTERS = 0x2
 XGR_CFG_NO_SPARSE_KERNEL = 0x4
 XGR_CFG_TIMING = 0x8
+XGR_CFG_PAPER_HEAP = 0x10   # baseline: the paper's per-beam Top-K lists + sequential heap
 XGR_NUM_COUNTERS = 8
 COUNTER_NAMES = ["rows_read", "rows_skip_pre", "rows_skip_post", "legal", "survivors",
                  "overflow", "sparse_cands", "dense_steps"]

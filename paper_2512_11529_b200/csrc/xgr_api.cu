@@ -48,6 +48,8 @@ struct xgr_ctx {
   int32_t** d_thist = nullptr;
   uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
   uint32_t* next_keys[2] = {nullptr, nullptr};   // per-request next-step candidates (route), by step parity
+  uint64_t* ph_lists = nullptr;    // XGR_CFG_PAPER_HEAP: [maxB][BW][K] per-beam sorted Top-K
+  int32_t* ph_cnt = nullptr;       // [maxB][BW]
   uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
   float* head_logits = nullptr;    // [maxB][kSparseCap]: legal logits of a fused-head sparse step
   uint64_t* surv = nullptr;        // [maxB][cap]
@@ -123,6 +125,8 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->d_phist);
   cudaFree(c->d_thist);
   cudaFree(c->scratch);
+  cudaFree(c->ph_lists);
+  cudaFree(c->ph_cnt);
   cudaFree(c->next_keys[0]);
   cudaFree(c->next_keys[1]);
   cudaFree(c->seed_hist);
@@ -182,7 +186,9 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.survivor_cap < 0 || c.theta_rows < 0) return fail(XGR_ERR_INVALID_ARG, "init: negative knob");
   for (int i = 0; i < 5; ++i)
     if (c.reserved[i]) return fail(XGR_ERR_INVALID_ARG, "init: reserved fields must be zero");
-  if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL | XGR_CFG_TIMING))
+  if ((c.flags & XGR_CFG_PAPER_HEAP) && (c.vocab > 16384 || c.nranks > 1))
+    return fail(XGR_ERR_UNSUPPORTED, "init: the paper-heap baseline needs vocab <= 16384 and no codebook shard");
+  if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL | XGR_CFG_TIMING | XGR_CFG_PAPER_HEAP))
     return fail(XGR_ERR_INVALID_ARG, "init: unknown flags 0x%x", c.flags);
   int ndev = 0;
   ACK(cudaGetDeviceCount(&ndev));
@@ -223,6 +229,11 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->d_phist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->d_thist, x->nd * sizeof(void*));
   if (e == cudaSuccess) e = al((void**)&x->scratch, 3 * (size_t)x->maxB * 4);
+  if (e == cudaSuccess && (c.flags & XGR_CFG_PAPER_HEAP)) {
+    const size_t K = x->K ? x->K : x->BW;
+    e = al((void**)&x->ph_lists, nb * K * 8);
+    if (e == cudaSuccess) e = al((void**)&x->ph_cnt, nb * 4);
+  }
   if (e == cudaSuccess) e = al((void**)&x->next_keys[0], (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->next_keys[1], (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
@@ -353,6 +364,8 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   a.token_out = ctx->token_hist + (size_t)(t - 1) * nb;
   // the commit counts each request's next-step candidates only when that step can be mixed
   if (t < ctx->nd && may_mix(ctx, t + 1)) a.next_keys_out = ctx->next_keys[t & 1];
+  a.ph_lists = ctx->ph_lists;
+  a.ph_cnt = ctx->ph_cnt;
   if (t > 1) a.next_keys_in = ctx->next_keys[(t - 1) & 1];
   a.theta = ctx->scratch;
   a.surv_count = ctx->scratch + ctx->maxB;
@@ -405,7 +418,7 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   const LevelHost& lv = ctx->trie.lv[t - 1];
   const bool has_sparse_nodes = lv.n_dense < lv.n_nodes;
   const bool streamed = stream_supported(ctx->V);
-  if (!sparse_route && streamed && has_sparse_nodes) {
+  if (!sparse_route && streamed && has_sparse_nodes && !ctx->ph_lists) {
     a.defer_sparse = 1;
     a.mixed = may_mix(ctx, t) ? 1 : 0;
   }

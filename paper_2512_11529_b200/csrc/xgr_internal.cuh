@@ -124,6 +124,9 @@ struct StepArgs {
   uint32_t* next_keys_out;        // this step's commit [batch] (null at the last step)
   int32_t mixed;                  // 1: both routes launched this step
   int32_t defer_sparse;           // 1: k_stream leaves sparse-parent rows to k_sparse_rows
+  // paper-heap baseline (XGR_CFG_PAPER_HEAP): per-beam sorted Top-K lists [batch][BW][K] and counts
+  uint64_t* ph_lists;
+  int32_t* ph_cnt;
   // codebook shard (nranks > 1): this rank's logits hold columns [col0, col0 + Vl) of V
   int32_t col0;
   int32_t Vl;

@@ -1535,6 +1535,152 @@ __global__ void __launch_bounds__(128) k_sparse_stats(const __grid_constant__ St
 }
 
 // ---------------------------------------------------------------------------------------------
+// The paper's own selection procedure on the GPU (SURVEY 8(f) f3 "paper-heap GPU variant"): an
+// in-repo baseline for the threshold-pruned design, selected with XGR_CFG_PAPER_HEAP at init. It
+// computes the same result (the heap is exact), the way PAPER.md section 6.2 describes it:
+//  * L156 / L376: each beam's Top-K candidates, sorted descending ("the log_prob results for each
+//    beam are inherently in descending order") -- k_ph_rows, one CTA per (request, beam): the beam's
+//    legal logits, log-softmax, every candidate key in shared memory, exact block Top-K (radix
+//    select + sort), written to a per-beam list;
+//  * L385: "a global min heap of size BW ... visits the leaves of each sub-beam tree sequentially
+//    ... if the leaf's log_prob exceeds that of the heap's top element, it is inserted ...
+//    Otherwise, the sorting operation of that beam is terminated immediately" -- k_ph_heap, one CTA
+//    per request whose first thread runs the heap sequentially (with the sorted-beam-score stop of
+//    SURVEY 8(c.2)); the heap is then sorted and committed like any step.
+// Only dense-route steps take it (the paper's sorting bottleneck); sparse steps are unchanged.
+// ---------------------------------------------------------------------------------------------
+template <int T, typename TI>
+__global__ void __launch_bounds__(T) k_ph_rows(const __grid_constant__ StepArgs a) {
+  extern __shared__ __align__(16) uint64_t s_k[];   // [V] candidate keys of the beam
+  __shared__ uint64_t s_sel[kMaxBW], s_out[kMaxBW];
+  __shared__ TopkScratch s_sc;
+  __shared__ float s_red[T / 32], s_red2[T / 32];
+  __shared__ uint32_t s_n;
+  const int req = blockIdx.x, b = blockIdx.y, tid = threadIdx.x;
+  const int K = a.topk ? a.topk : a.BW;
+  uint64_t* lst = a.ph_lists + ((size_t)req * a.BW + b) * K;
+  if (b >= nlive_of(a, req)) {
+    if (tid == 0) a.ph_cnt[(size_t)req * a.BW + b] = 0;
+    return;
+  }
+  float S;
+  uint32_t node;
+  row_state(a, req, b, S, node);
+  const LevelDev& L = a.trie.lv[a.level];
+  const uint16_t* lab = a.trie.lv[a.level + 1].label;
+  const uint32_t fc = L.first_child[node], fe = L.first_child[node + 1];
+  const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
+  // the beam's legal logits (its children in label order)
+  float tm = -INFINITY;
+  for (uint32_t q = fc + tid; q < fe; q += T) tm = fmaxf(tm, ldx(row + lab[q]));
+  const float M = block_max<T>(tm, s_red);
+  float z = 0.f;
+  for (uint32_t q = fc + tid; q < fe; q += T) z += ex2(__fmul_rn(__fsub_rn(ldx(row + lab[q]), M), kLog2e));
+  const float Z = block_sum<T>(z, s_red2);
+  const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+  const float lse = row_lse(M, Z);
+  if (!finite && tid == 0) atomicOr(a.flags + req, kFlagNonfinite);
+  const uint32_t fbase = (uint32_t)b * (uint32_t)a.trie.V;
+  const int n = (int)(fe - fc);
+  for (int i = tid; i < n; i += T) {
+    const uint32_t v = lab[fc + i];
+    s_k[i] = make_key(cand_score(S, ldx(row + v), lse), fbase + v);
+  }
+  __syncthreads();
+  const int k = min(n, K);
+  if (k < n) {
+    block_select_topk<T>(s_k, n, k, s_sel, s_out, s_sc.hist, s_sc.m64, s_sc.m32);
+  } else {
+    for (int i = tid; i < n; i += T) s_sel[i] = s_k[i];
+    __syncthreads();
+    sort_desc_to<T>(s_sel, n, s_out);
+  }
+  for (int i = tid; i < k; i += T) lst[i] = s_out[i];
+  if (tid == 0) a.ph_cnt[(size_t)req * a.BW + b] = k;
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) k_ph_heap(const __grid_constant__ StepArgs a) {
+  __shared__ uint64_t s_heap[kMaxBW], s_out[kMaxBW];
+  __shared__ ParentInfo s_pi;
+  __shared__ int s_hn;
+  const int req = blockIdx.x, tid = threadIdx.x;
+  const int nl = nlive_of(a, req), BW = a.BW;
+  const int K = a.topk ? a.topk : a.BW;
+  prefetch_parents<T>(a, req, nl, s_pi);
+  if (tid == 0) {
+    // min-heap of keys (a larger key is a better candidate: score desc, flat asc)
+    int hn = 0;
+    uint64_t visits = 0;
+    for (int b = 0; b < nl; ++b) {
+      float S;
+      uint32_t node;
+      row_state(a, req, b, S, node);
+      // every candidate of beam b and of later beams is <= S_b, and later beams have larger flat
+      // indices: once the heap is full and S_b <= its minimum score nothing can enter any more
+      if (hn == BW && !(S > key_score(s_heap[0]))) break;
+      const uint64_t* lst = a.ph_lists + ((size_t)req * BW + b) * K;
+      const int cnt = a.ph_cnt[(size_t)req * BW + b];
+      for (int i = 0; i < cnt; ++i) {
+        const uint64_t key = lst[i];
+        ++visits;
+        if (hn < BW) {   // push, sift up
+          int j = hn++;
+          while (j > 0) {
+            const int p = (j - 1) >> 1;
+            if (s_heap[p] <= key) break;
+            s_heap[j] = s_heap[p];
+            j = p;
+          }
+          s_heap[j] = key;
+        } else if (key > s_heap[0]) {   // replace the minimum, sift down
+          int j = 0;
+          for (;;) {
+            const int l = 2 * j + 1, r = l + 1;
+            int m = j;
+            uint64_t mv = key;
+            if (l < hn && s_heap[l] < mv) { m = l; mv = s_heap[l]; }
+            if (r < hn && s_heap[r] < mv) { m = r; mv = s_heap[r]; }
+            if (m == j) break;
+            s_heap[j] = s_heap[m];
+            j = m;
+          }
+          s_heap[j] = key;
+        } else {
+          break;   // the beam's traversal terminates
+        }
+      }
+    }
+    s_hn = hn;
+    count_add(a, XGR_CNT_SURVIVORS, visits);   // heap visits (the paper's sorting work)
+  }
+  __syncthreads();
+  const int hn = s_hn;
+  sort_desc_to<T>(s_heap, hn, s_out);
+  commit<T>(a, req, s_out, hn, s_pi);
+}
+
+cudaError_t launch_paper_heap(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                              int* launches) {
+  const size_t smem = (size_t)a.trie.V * sizeof(uint64_t);
+  cudaError_t e;
+  if (a.dtype == XGR_DTYPE_BF16) {
+    if ((e = cudaFuncSetAttribute(k_ph_rows<512, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem)))
+      return e;
+  } else if ((e = cudaFuncSetAttribute(k_ph_rows<512, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) {
+    return e;
+  }
+  if (ev0) cudaEventRecord(ev0, s);
+  if (a.dtype == XGR_DTYPE_BF16) launch_pdl(k_ph_rows<512, __nv_bfloat16>, dim3(a.batch, rows), 512, smem, s, a);
+  else launch_pdl(k_ph_rows<512, float>, dim3(a.batch, rows), 512, smem, s, a);
+  launch_pdl(k_ph_heap<256>, a.batch, 256, 0, s, a);
+  if (ev1) cudaEventRecord(ev1, s);
+  *launches += 2;
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
 // support: children of prefixes, read from the representation the step kernels use.
 // ---------------------------------------------------------------------------------------------
 __global__ void k_children(TrieDev tr, const int32_t* prefixes, int depth, int64_t n, int32_t* counts,
@@ -1692,6 +1838,7 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
                         cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1, int* launches) {
   cudaError_t e;
   const bool bf16 = a.dtype == XGR_DTYPE_BF16;
+  if (a.ph_lists && !sparse_route) return launch_paper_heap(a, rows, s, ev0, ev1, launches);
   if (a.mixed) {
     // both routes: k_sparse commits the requests whose next-step candidates fit on chip (decided
     // per request by the previous commit), the dense path the others (it skips the former); the

@@ -1021,7 +1021,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   for (int k = g;; k += G) {
     if (!row_ok(k)) break;
     const int st = R::stage(k);
-    mbar_wait(&full[st], R::use(k) & 1);
+    // consumers wait for their stage with a suspend-time hint (no busy polling that would take
+    // issue slots from the other groups of the SM); XGR_DEBUG_FLAGS bit 23: plain polling (A/B)
+    if (a.dbg & (1 << 23)) mbar_wait(&full[st], R::use(k) & 1);
+    else mbar_wait_sleep(&full[st], R::use(k) & 1);
     // the row descriptor
     Desc d;
     float th;
@@ -1450,8 +1453,9 @@ static size_t stream_smem() {
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
-static int g_seed_kernel = 0;      // XGR_SEED_KERNEL: 0 request-major seed with theta (k_stream kModeSeedReq),
-                                   // 1 k_seed_hist + k_seed_theta, 2 b-major streamed seed + k_seed_theta
+static int g_seed_kernel = 2;      // XGR_SEED_KERNEL: 2 b-major streamed seed + k_seed_theta (default),
+                                   // 0 request-major seed with theta in the same kernel (as fast at C3,
+                                   // slower at C2: one CTA per request), 1 k_seed_hist + k_seed_theta
 static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>

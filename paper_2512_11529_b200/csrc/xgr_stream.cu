@@ -1476,7 +1476,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     if ((a.dbg & 1) == 0 && __any_sync(0xffffffffu, ns > 0)) {
       flush();
       const uint32_t fbase = (uint32_t)b * (uint32_t)V + (uint32_t)ccol;
-      if (C > 1 || __any_sync(0xffffffffu, ns > 2)) {
+      if (C > 1 || EPT > 32 || __any_sync(0xffffffffu, ns > 2)) {
         // many candidates in one lane (weak theta), or a cluster (registers for the deferred
         // exchange instead): reserve and write synchronously
         uint64_t* sbuf = a.surv + (size_t)req * a.cap;
@@ -1716,6 +1716,12 @@ cudaError_t configure_stream_kernels() {
   if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 3, 2, kModeSeedReq>, stream_smem<32, 3>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<64, 2, 4, 2, kModeNormal, __nv_bfloat16, 128>, stream_smem<64, 4, __nv_bfloat16, 128>())) !=
+      cudaSuccess)
+    return e;
+  if ((e = opt_in(k_stream<64, 1, 2, 4, kModeNormal, __nv_bfloat16, 128>, stream_smem<64, 2, __nv_bfloat16, 128>())) !=
+      cudaSuccess)
+    return e;
   if ((e = opt_in(k_stream<32, 1, 4, 2, kModeSeedReq, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
       cudaSuccess)
     return e;
@@ -1784,7 +1790,13 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     }
     if (ev0) cudaEventRecord(ev0, s);
-    if (a.trie.V <= 8192)
+    if (a.trie.V <= 8192 && g_stream_variant == 4)   // 128-thread groups, 64 tokens per thread, 2 groups per CTA
+      launch_pdl(k_stream<64, 2, 4, 2, kModeNormal, bf, 128>, std::min(total, 2 * sms), 2 * 128 + 32,
+                 stream_smem<64, 4, bf, 128>(), s, a, total, 0);
+    else if (a.trie.V <= 8192 && g_stream_variant == 5)   // 128-thread groups, one per CTA, 4 CTAs per SM
+      launch_pdl(k_stream<64, 1, 2, 4, kModeNormal, bf, 128>, std::min(total, 4 * sms), 128 + 32,
+                 stream_smem<64, 2, bf, 128>(), s, a, total, 0);
+    else if (a.trie.V <= 8192)
       launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s,
           a, total, 0);
     else   // 16384-token rows: one 512-thread consumer group per SM, 4 x 32 KB stages

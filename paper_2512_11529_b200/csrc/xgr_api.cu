@@ -12,7 +12,15 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3: a no-op unless a profiler is attached
+
 #include "xgr_internal.cuh"
+
+// NVTX range over one ABI call (nsys / ncu --nvtx timelines show the host calls per step)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 namespace xgr {
 cudaError_t configure_kernels(int cap);
@@ -281,6 +289,7 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
 }
 
 xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, void* stream) {
+  NvtxRange nvtx_("xgr_mask_build");
   if (!ctx) return fail(XGR_ERR_INVALID_ARG, "mask_build: ctx is NULL");
   if (ctx->built) return fail(XGR_ERR_SEQUENCE, "mask_build: trie already built");
   if (n_items < 0) return fail(XGR_ERR_INVALID_ARG, "mask_build: n_items < 0");
@@ -397,6 +406,7 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
 
 xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype, int32_t rows,
                             int64_t ld, void* stream) {
+  NvtxRange nvtx_("xgr_beam_step_ex");
   StepArgs a;
   int rows_live = 0;
   xgr_status st = step_args(ctx, batch, logits, dtype, rows, ld, "step", a, rows_live);
@@ -464,6 +474,7 @@ xgr_status xgr_beam_next_route(const xgr_ctx* ctx, int32_t* sparse) {
 
 xgr_status xgr_beam_step_head(xgr_ctx* ctx, int32_t batch, const void* hidden, int32_t rows, int64_t ldh,
                               const void* head, int64_t ldw, const float* bias, int32_t d, void* stream) {
+  NvtxRange nvtx_("xgr_beam_step_head");
   if (!ctx) return fail(XGR_ERR_INVALID_ARG, "step_head: ctx is NULL");
   if (d < 8 || (d & 7) || ldw < d || (ldw & 7))
     return fail(XGR_ERR_INVALID_ARG, "step_head: d %d (a multiple of 8) and ldw %lld >= d (multiple of 8)", d,
@@ -497,6 +508,7 @@ xgr_status xgr_beam_step_head(xgr_ctx* ctx, int32_t batch, const void* hidden, i
 // ---- codebook shard: stats -> (all-gather) -> select -> (all-gather) -> merge -------------------
 xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows, int64_t ld,
                            void* stream, const float** stats) {
+  NvtxRange nvtx_("xgr_shard_stats");
   StepArgs a;
   int rows_live = 0;
   xgr_status st = step_args(ctx, batch, logits, XGR_DTYPE_F32, rows, ld, "shard_stats", a, rows_live);
@@ -523,6 +535,7 @@ xgr_status xgr_shard_stats(xgr_ctx* ctx, int32_t batch, const float* logits, int
 
 xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, const uint64_t** recs,
                             const int32_t** rec_n) {
+  NvtxRange nvtx_("xgr_shard_select");
   if (!ctx || !gstats || !recs || !rec_n) return fail(XGR_ERR_INVALID_ARG, "shard_select: NULL argument");
   if (ctx->shard_phase != 1) return fail(XGR_ERR_SEQUENCE, "shard_select: call shard_stats first");
   StepArgs a = ctx->shard_args;
@@ -547,6 +560,7 @@ xgr_status xgr_shard_select(xgr_ctx* ctx, const float* gstats, void* stream, con
 }
 
 xgr_status xgr_shard_merge(xgr_ctx* ctx, const uint64_t* grecs, const int32_t* grec_n, void* stream) {
+  NvtxRange nvtx_("xgr_shard_merge");
   if (!ctx || !grecs) return fail(XGR_ERR_INVALID_ARG, "shard_merge: NULL argument");
   if (ctx->shard_phase != 2) return fail(XGR_ERR_SEQUENCE, "shard_merge: call shard_select first");
   StepArgs a = ctx->shard_args;
@@ -566,6 +580,7 @@ xgr_status xgr_shard_merge(xgr_ctx* ctx, const uint64_t* grecs, const int32_t* g
 
 xgr_status xgr_beam_finalize(xgr_ctx* ctx, int32_t* tokens, int64_t* item_rank, float* score,
                              int32_t* n_live, int32_t outputs_on_device, void* stream) {
+  NvtxRange nvtx_("xgr_beam_finalize");
   if (!ctx) return fail(XGR_ERR_INVALID_ARG, "finalize: ctx is NULL");
   if (ctx->step != ctx->nd)
     return fail(XGR_ERR_SEQUENCE, "finalize: %d of %d steps done", ctx->step, ctx->nd);

@@ -1373,6 +1373,41 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
       const float lse3 = row_lse(M, Z);
       const float S0 = d.lse;
+      const int mm = (BW + GT / 32 - 1) / (GT / 32);
+      if (mm <= 32 && !(a.dbg & (1 << 24))) {
+        // BW <= GT: each warp's bound is the minimum of its lanes' maxima (over lanes holding a legal
+        // token), so every such lane has a candidate >= it; if the row's warps vouch for >= BW
+        // candidates this way, count those >= their warp's bound (found by groups of 4 on the raw
+        // logits: c is increasing in x). Counting only real candidates keeps theta valid whatever
+        // the bound; the bound only limits the atomics. Otherwise the top-2 path below.
+        const bool has = tmax > -INFINITY;
+        const float wmin = -wmax(has ? -tmax : -INFINITY);
+        const int nw = __popc(__ballot_sync(0xffffffffu, has));
+        if (lane == 0) p_sum[g][lt >> 5] = __int_as_float(nw);   // (s_tau is the fallback's)
+        named_sync(bar_id, GT);
+        int tot = 0;
+#pragma unroll
+        for (int w2 = 0; w2 < GT / 32; ++w2) tot += __float_as_int(p_sum[g][w2]);
+        if (tot >= BW) {
+          if (has) {
+            uint32_t* h = SREQ ? s_hist : a.seed_hist + (size_t)req * kSeedBins;
+#pragma unroll
+            for (int i = 0; i < EPT / 4; ++i) {
+              const float m4 = fmaxf(fmaxf(x[4 * i], x[4 * i + 1]), fmaxf(x[4 * i + 2], x[4 * i + 3]));
+              if (m4 >= wmin) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                  if (x[4 * i + j] >= wmin && x[4 * i + j] > -INFINITY) {
+                    const float dd = __fmul_rn(__fsub_rn(S0, cand_score(S, x[4 * i + j], lse3)), 128.0f);
+                    if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(h + (int)dd, 1u);
+                  }
+                }
+              }
+            }
+          }
+          continue;
+        }
+      }
       float c1 = -INFINITY, c2 = -INFINITY;
 #pragma unroll
       for (int e = 0; e < EPT; ++e) {
@@ -1380,7 +1415,6 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         c2 = fmaxf(c2, fminf(c1, x[e]));
         c1 = fmaxf(c1, x[e]);
       }
-      const int mm = (BW + GT / 32 - 1) / (GT / 32);
       float tau = -INFINITY;
       if (mm <= 64) {
         float A = c1, B = c2;

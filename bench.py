@@ -545,6 +545,15 @@ def account(args, cfg, plan, dev, items, logits, main_ms, dense_steps, per_step,
             "dense_step_ms_p50": step_dense,
             "dense_step_frac": (algb["alg_bytes"] / (step_dense / 1e3) / 1e9 / peak) if step_dense else None,
         }
+        rr = counters.get("rows_read")
+        if rr:
+            # bytes of the rows the kernel actually read (rows not skipped before reading: the
+            # seed's theta is weaker than theta*, so this exceeds the algorithmic bytes at sigma 4)
+            esz = 2 if args.logits == "bf16" else 4
+            vl = cfg["vocab"] // (SHARDS if shard else 1)
+            rbytes = rr * (vl * esz + vl // 8 + 16)
+            out["roofline"]["rows_read_bytes_per_launch"] = rbytes
+            out["roofline"]["frac_rows_read"] = rbytes / (mean_ms / 1e3) / 1e9 / peak
         if shard:
             out["roofline"]["note"] = ("the shard select phase re-reads the rows after the stats all-gather "
                                        "(the global lse is needed before any emission), so the dense step "

@@ -1363,7 +1363,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       }
     }
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
-      if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+      if (lt == 0) {
+        a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
+        if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
+      }
       continue;
     }
     if (SEED) {

@@ -1018,75 +1018,6 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
   };
   int xit = 0;   // dense rows exchanged within the cluster (mailbox slot / phase)
-  // Cluster, main pass: the exchange of row k is consumed one row later. Every CTA selects its
-  // slice's candidates with its LOCAL lse_r <= lse (a superset: c = S + x - lse <= S + x - lse_r),
-  // keeps at most two per thread in registers, and scores them exactly with the global lse while
-  // the next row is in flight; a warp with more waits for the exchange at once (resolve below).
-  // the row-level facts of the last two exchanged rows live in shared memory (written by thread 0
-  // of the group, read one row later after the group barrier); per thread only its candidates
-  struct DRow {
-    int req, b;
-    float S, th;
-  };
-  __shared__ DRow s_drow[2];
-  int dp_n = -1;          // this warp's deferred row: -1 none, else this thread's candidate count
-  float dp_x0 = 0.f, dp_x1 = 0.f;
-  uint32_t dp_v = 0;      // the two candidates' columns (16 bits each; V <= 65536)
-  int dp_x = 0;           // the deferred row's exchange index
-  // global (M, Z) of the row in mailbox slot xs (identical on every CTA: rank-order combine)
-  auto xcombine = [&](int xs, float& Mg, float& Zg) {   // two passes over the mailbox (registers)
-    Mg = mbox[xs][0].x;
-#pragma unroll 1
-    for (int r = 1; r < C; ++r) Mg = fmaxf(Mg, mbox[xs][r].x);
-    Zg = 0.f;
-#pragma unroll 1
-    for (int r = 0; r < C; ++r) {
-      const float2 q = mbox[xs][r];
-      if (q.y > 0.f) Zg = __fadd_rn(Zg, __fmul_rn(q.y, ex2f(__fmul_rn(__fsub_rn(q.x, Mg), kLog2eS))));
-      else if (q.y != q.y) Zg = q.y;
-    }
-  };
-  auto resolve = [&]() {
-    if (dp_n < 0) return;
-    const int dp_xs = dp_x % NXS;
-    const DRow dr = s_drow[dp_x & 1];
-    const int dp_req = dr.req, dp_b = dr.b;
-    const float dp_S = dr.S, dp_th = dr.th;
-    const uint32_t dp_v0 = dp_v & 0xFFFFu, dp_v1 = dp_v >> 16;
-    mbar_wait(&xbar[dp_xs], (uint32_t)(dp_x / NXS) & 1u);
-    float Mg, Zg;
-    xcombine(dp_xs, Mg, Zg);
-    const bool fin = (Zg > 0.5f) && (Zg <= 3.0e38f);
-    const float lse = row_lse(Mg, Zg);
-    const bool ub = fin && cand_score(dp_S, Mg, lse) >= dp_th;
-    if (lt == 0 && crank == 0) {
-      a.lse[(size_t)dp_req * BW + dp_b] = fin ? lse : __int_as_float(0x7fc00000);
-      if (!fin) atomicOr(a.flags + dp_req, kFlagNonfinite);
-      if (a.counters_on) {
-        atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
-        if (fin && !ub) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
-      }
-    }
-    const uint32_t fbase = (uint32_t)dp_b * (uint32_t)V;
-    const float c0 = cand_score(dp_S, dp_x0, lse), c1 = cand_score(dp_S, dp_x1, lse);
-    const bool t0 = ub && dp_n > 0 && c0 >= dp_th, t1 = ub && dp_n > 1 && c1 >= dp_th;
-    const uint32_t nt = (uint32_t)t0 + (uint32_t)t1;
-    if (__any_sync(0xffffffffu, nt > 0)) {
-      flush();
-      uint32_t pos = warp_reserve(nt, a.surv_count + dp_req);
-      uint64_t* sbuf = a.surv + (size_t)dp_req * a.cap;
-      if (t0) {
-        if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(c0, fbase + dp_v0);
-        ++pos;
-      }
-      if (t1 && pos < (uint32_t)a.cap) sbuf[pos] = make_key(c1, fbase + dp_v1);
-    }
-    if (a.counters_on) {
-      const int tot = __reduce_add_sync(0xffffffffu, (int)nt);
-      if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
-    }
-    dp_n = -1;
-  };
   for (int k = g;; k += G) {
     if (!row_ok(k)) break;
     const int st = R::stage(k);
@@ -1273,66 +1204,6 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 #pragma unroll
     for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
     float Z = __shfl_sync(0xffffffffu, zi, 0);
-    if constexpr (C > 1 && MODE == kModeNormal) {
-      const int xs = xit % NXS;
-      const uint32_t ph = (uint32_t)(xit / NXS) & 1u;
-      const int xcur = xit++;
-      if (lt == 0) {   // this slice's (m, Z) to every CTA of the cluster (see the blocking path below)
-        s_drow[xcur & 1] = DRow{req, b, S, th};
-        mbar_arrive_tx(&xbar[xs], 8u * C);
-        const float2 mine2 = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
-#pragma unroll 1
-        for (int r = 0; r < C; ++r)
-          st_async_f2(mapa(smem_u32(&mbox[xs][crank]), (uint32_t)r), mine2, mapa(smem_u32(&xbar[xs]), (uint32_t)r));
-      }
-      resolve();   // the previous row: its partials have had a row's time to arrive
-      // this row's superset candidates under the local lse_r (a slice without legal tokens has none)
-      const bool lfin = (Z > 0.5f) && (Z <= 3.0e38f);
-      const float lse_r = row_lse(M, Z);
-      int n = 0;
-      float x0 = 0.f, x1 = 0.f;
-      uint32_t v0 = 0, v1 = 0;
-      bool now = th == -INFINITY;   // no bound: every legal token is a candidate
-      if (lfin && !now && cand_score(S, M, lse_r) >= th) {
-        const float xthr = (th - S) + lse_r - 1e-5f * (fabsf(th) + fabsf(S) + 2.0f * fabsf(lse_r));
-        if (tmax >= xthr) {
-#pragma unroll
-          for (int e = 0; e < EPT; ++e) {
-            if (x[e] >= xthr) {
-              const uint32_t v = (uint32_t)CH * (uint32_t)((e / CH) * GT + lt) + (uint32_t)(e % CH) + (uint32_t)ccol;
-              if (n == 0) { x0 = x[e]; v0 = v; } else if (n == 1) { x1 = x[e]; v1 = v; }
-              ++n;
-            }
-          }
-        }
-      }
-      now = now || n > 2;
-      if (!__any_sync(0xffffffffu, now)) {   // defer this row
-        dp_n = n;
-        dp_x = xcur;
-        dp_x0 = x0;
-        dp_x1 = x1;
-        dp_v = v0 | (v1 << 16);
-        continue;
-      }
-      // this warp resolves the row now: wait for the exchange and emit exactly below (the other
-      // warps of the group may defer it; every warp consumes the slot before its peers reuse it)
-      mbar_wait(&xbar[xs], ph);
-      xcombine(xs, M, Z);
-      if (!((Z > 0.5f) && (Z <= 3.0e38f))) {
-        if (lt == 0 && crank == 0) {
-          a.lse[(size_t)req * BW + b] = __int_as_float(0x7fc00000);
-          atomicOr(a.flags + req, kFlagNonfinite);
-        }
-        continue;
-      }
-      lse = row_lse(M, Z);
-      if (lt == 0 && crank == 0) {
-        a.lse[(size_t)req * BW + b] = lse;
-        if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
-      }
-      if (!(cand_score(S, M, lse) >= th)) continue;
-    } else {
     if constexpr (C > 1) {
       // this slice's (m, Z) to every CTA of the cluster (slot xit % NXS), then the C partials
       // combined in rank order: M = max_r m_r, Z = sum_r Z_r 2^((m_r - M) log2 e) -- identical on
@@ -1349,17 +1220,15 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       }
       mbar_wait(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
       ++xit;
-      float2 q[C];
-#pragma unroll
-      for (int r = 0; r < C; ++r) q[r] = mbox[xs][r];
-      M = q[0].x;
-#pragma unroll
-      for (int r = 1; r < C; ++r) M = fmaxf(M, q[r].x);
+      M = mbox[xs][0].x;   // two passes over the mailbox (no register array for the C partials)
+#pragma unroll 1
+      for (int r = 1; r < C; ++r) M = fmaxf(M, mbox[xs][r].x);
       Z = 0.f;
-#pragma unroll
+#pragma unroll 1
       for (int r = 0; r < C; ++r) {
-        if (q[r].y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q[r].y, ex2f(__fmul_rn(__fsub_rn(q[r].x, M), kLog2eS))));
-        else if (q[r].y != q[r].y) Z = q[r].y;
+        const float2 q = mbox[xs][r];
+        if (q.y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q.y, ex2f(__fmul_rn(__fsub_rn(q.x, M), kLog2eS))));
+        else if (q.y != q.y) Z = q.y;
       }
     }
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
@@ -1478,7 +1347,6 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (lt == 0 && crank == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
     }
-    }   // blocking path
     }   // MODE != kModeShardEmit
     // select this thread's candidates (bit e of `mine`), then one atomic per warp reserves slots
     uint64_t mine = 0ull;
@@ -1513,9 +1381,9 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     if ((a.dbg & 1) == 0 && __any_sync(0xffffffffu, ns > 0)) {
       flush();
       const uint32_t fbase = (uint32_t)b * (uint32_t)V + (uint32_t)ccol;
-      if (C > 1 || EPT > 32 || __any_sync(0xffffffffu, ns > 2)) {
-        // many candidates in one lane (weak theta), or a cluster (registers for the deferred
-        // exchange instead): reserve and write synchronously
+      if (EPT > 32 || __any_sync(0xffffffffu, ns > 2)) {
+        // many candidates in one lane (weak theta), or 64 tokens per thread (the registers of the
+        // deferred reservation): reserve and write synchronously
         uint64_t* sbuf = a.surv + (size_t)req * a.cap;
         uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + req);
 #pragma unroll
@@ -1561,7 +1429,6 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
     }
   }
-  if constexpr (C > 1 && MODE == kModeNormal) resolve();
   flush();
   if constexpr (SREQ) {
     // theta of request blockIdx.x from its histogram of d = S_0 - c (bins of 1/128): the first bin

@@ -822,6 +822,8 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   constexpr int NCH = EPT / CH;               // chunks per thread
   constexpr uint32_t CHM = (1u << CH) - 1u;   // a chunk's mask bits
   constexpr int NC = GT * G;       // consumer threads
+  // fp32 rows of 32 tokens per thread use the rotated layout (one mask word per thread per row)
+  constexpr bool ROT = EPT == 32 && sizeof(TI) == 4;
   extern __shared__ __align__(128) unsigned char s_dynb[];
   TI* s_row = reinterpret_cast<TI*>(s_dynb);                                         // [NS][VT]
   uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dynb + (size_t)NS * VT * sizeof(TI));  // [NS][MW]
@@ -977,6 +979,11 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 
   // ------------------------------- consumer groups ----------------------------------------
   const int g = tid / GT, lt = tid - g * GT, lane = tid & 31;
+  // column (within this CTA's slice) of this thread's x[e]
+  auto tok = [&](int e) -> uint32_t {
+    if constexpr (ROT) return 32u * lt + 4u * (uint32_t)(((e >> 2) + lt) & 7) + (uint32_t)(e & 3);
+    else return (uint32_t)CH * (uint32_t)((e / CH) * GT + lt) + (uint32_t)(e % CH);
+  };
   const int bar_id = 1 + g;
   const uint16_t* lab = a.trie.lv[a.level + 1].label;
   float* pmax = p_max[g];
@@ -1139,18 +1146,36 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     // ---- dense row: stage -> registers. Thread lt owns the 16-byte chunks q = i*GT + lt
     // (i < NCH; CH tokens each): consecutive per lane, conflict-free, compile-time offsets; its
     // mask bits are CH*(lt % (32/CH)) .. +CH-1 of word q*CH/32 = i*GT*CH/32 + lt/(32/CH).
-    const TI* srow = s_row + (size_t)st * VT + CH * lt;
-    const uint32_t* smsk = s_msk + (size_t)st * MW + (lt / (32 / CH));
     const int nsh = CH * (lt & (32 / CH - 1));
     float x[EPT];
+    if constexpr (ROT) {
+      // thread lt owns tokens [32 lt, 32 lt + 32) (mask word lt, one shared load); its chunk i is
+      // the float4 (i + lt) & 7 of that range: within each 8-lane phase of an LDS.128 the lanes hit
+      // distinct bank groups
+      const float* srow = reinterpret_cast<const float*>(s_row) + (size_t)st * VT + 32 * lt;
+      const uint32_t w = s_msk[(size_t)st * MW + lt];
+      const uint32_t wrot = __funnelshift_r(w, w, 4 * (lt & 7));   // nibble i: chunk i
 #pragma unroll
-    for (int i = 0; i < NCH; ++i) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(srow + i * GT * CH);
-      const uint32_t nb = smsk[i * (GT * CH / 32)] >> nsh;
-      float v[CH];
-      unpack_chunk<TI>(raw, v);
+      for (int i = 0; i < 8; ++i) {
+        const float4 raw = *reinterpret_cast<const float4*>(srow + 4 * ((i + lt) & 7));
+        const uint32_t nb = wrot >> (4 * i);
+        x[4 * i + 0] = (nb & 1u) ? raw.x : -INFINITY;
+        x[4 * i + 1] = (nb & 2u) ? raw.y : -INFINITY;
+        x[4 * i + 2] = (nb & 4u) ? raw.z : -INFINITY;
+        x[4 * i + 3] = (nb & 8u) ? raw.w : -INFINITY;
+      }
+    } else {
+      const TI* srow = s_row + (size_t)st * VT + CH * lt;
+      const uint32_t* smsk = s_msk + (size_t)st * MW + (lt / (32 / CH));
 #pragma unroll
-      for (int j = 0; j < CH; ++j) x[CH * i + j] = ((nb >> j) & 1u) ? v[j] : -INFINITY;
+      for (int i = 0; i < NCH; ++i) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(srow + i * GT * CH);
+        const uint32_t nb = smsk[i * (GT * CH / 32)] >> nsh;
+        float v[CH];
+        unpack_chunk<TI>(raw, v);
+#pragma unroll
+        for (int j = 0; j < CH; ++j) x[CH * i + j] = ((nb >> j) & 1u) ? v[j] : -INFINITY;
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
@@ -1369,12 +1394,17 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     } else {
       // no bound (pruning off or too few seed candidates): every legal token, -inf logits
       // included, is a candidate; legality re-read from the node's bitmap in global memory
-      const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (ccol >> 5) + (lt / (32 / CH));
+      if constexpr (ROT) {   // this thread's mask word from global memory, rotated like x[]
+        const uint32_t w = (32 * lt < Vc) ? __ldg(L.bitmap + (size_t)d.slot * W + (ccol >> 5) + lt) : 0u;
+        mine = (uint64_t)__funnelshift_r(w, w, 4 * (lt & 7));
+      } else {
+        const uint32_t* gm = L.bitmap + (size_t)d.slot * W + (ccol >> 5) + (lt / (32 / CH));
 #pragma unroll
-      for (int i = 0; i < NCH; ++i) {
-        const uint32_t q4 = (uint32_t)(i * GT + lt);
-        const uint32_t nb = (CH * q4 < (uint32_t)Vc) ? ((__ldg(gm + i * (GT * CH / 32)) >> nsh) & CHM) : 0u;
-        mine |= (uint64_t)nb << (CH * i);
+        for (int i = 0; i < NCH; ++i) {
+          const uint32_t q4 = (uint32_t)(i * GT + lt);
+          const uint32_t nb = (CH * q4 < (uint32_t)Vc) ? ((__ldg(gm + i * (GT * CH / 32)) >> nsh) & CHM) : 0u;
+          mine |= (uint64_t)nb << (CH * i);
+        }
       }
     }
     const int ns = __popcll(mine);
@@ -1389,7 +1419,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 #pragma unroll
         for (int e = 0; e < EPT; ++e) {
           if ((mine >> e) & 1ull) {
-            const uint32_t v = (uint32_t)CH * (uint32_t)((e / CH) * GT + lt) + (uint32_t)(e % CH);
+            const uint32_t v = tok(e);
             if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(S, x[e], lse), fbase + v);
             ++pos;
           }
@@ -1403,7 +1433,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 #pragma unroll
             for (int j = 0; j < CH; ++j) {
               if ((nb >> j) & 1u) {
-                const uint32_t v = (uint32_t)CH * (uint32_t)(i * GT + lt) + j;
+                const uint32_t v = tok(CH * i + j);
                 const uint64_t key = make_key(cand_score(S, x[CH * i + j], lse), fbase + v);
                 if (q == 0) pend_k0 = key; else pend_k1 = key;
                 ++q;

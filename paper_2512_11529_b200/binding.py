@@ -10,7 +10,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libxgr_beam.so")
+# XGR_LIB: an alternative build of the same library (development A/B builds only)
+LIB_PATH = os.environ.get("XGR_LIB") or os.path.join(_HERE, "lib", "libxgr_beam.so")
 
 XGR_OK = 0
 STATUS_NAMES = {

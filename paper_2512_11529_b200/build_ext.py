@@ -29,12 +29,14 @@ def _stale(objs) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, extra=()) -> str:
+def build(force: bool = False, verbose: bool = False, extra=(), lib: str = LIB) -> str:
+    """Compiles csrc/ into `lib` (default: the in-tree library); `extra`: additional nvcc flags
+    (a non-default `lib` with extra flags is an A/B build, e.g. -DXGR_NO_ROT)."""
     os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(LIBDIR, "obj")
+    objdir = os.path.join(LIBDIR, "obj" if lib == LIB else "obj_" + os.path.basename(lib).replace(".so", ""))
     os.makedirs(objdir, exist_ok=True)
     objs = [os.path.join(objdir, s.replace(".cu", ".o")) for s in SOURCES]
-    if not force and not _stale(objs):
+    if not force and lib == LIB and not _stale(objs):
         return LIB
 
     def compile_one(src_obj):
@@ -53,13 +55,13 @@ def build(force: bool = False, verbose: bool = False, extra=()) -> str:
         for lg in logs:
             if lg.strip():
                 print(lg)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

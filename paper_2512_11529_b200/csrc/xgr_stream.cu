@@ -823,7 +823,11 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   constexpr uint32_t CHM = (1u << CH) - 1u;   // a chunk's mask bits
   constexpr int NC = GT * G;       // consumer threads
   // fp32 rows of 32 tokens per thread use the rotated layout (one mask word per thread per row)
+#ifdef XGR_NO_ROT   // A/B builds only
+  constexpr bool ROT = false;
+#else
   constexpr bool ROT = EPT == 32 && sizeof(TI) == 4;
+#endif
   extern __shared__ __align__(128) unsigned char s_dynb[];
   TI* s_row = reinterpret_cast<TI*>(s_dynb);                                         // [NS][VT]
   uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dynb + (size_t)NS * VT * sizeof(TI));  // [NS][MW]
@@ -1245,15 +1249,17 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       }
       mbar_wait(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
       ++xit;
-      M = mbox[xs][0].x;   // two passes over the mailbox (no register array for the C partials)
-#pragma unroll 1
-      for (int r = 1; r < C; ++r) M = fmaxf(M, mbox[xs][r].x);
+      float2 q[C];   // all C partials loaded at once (the combine is on every row's critical path)
+#pragma unroll
+      for (int r = 0; r < C; ++r) q[r] = mbox[xs][r];
+      M = q[0].x;
+#pragma unroll
+      for (int r = 1; r < C; ++r) M = fmaxf(M, q[r].x);
       Z = 0.f;
-#pragma unroll 1
+#pragma unroll
       for (int r = 0; r < C; ++r) {
-        const float2 q = mbox[xs][r];
-        if (q.y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q.y, ex2f(__fmul_rn(__fsub_rn(q.x, M), kLog2eS))));
-        else if (q.y != q.y) Z = q.y;
+        if (q[r].y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q[r].y, ex2f(__fmul_rn(__fsub_rn(q[r].x, M), kLog2eS))));
+        else if (q[r].y != q[r].y) Z = q[r].y;
       }
     }
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)
@@ -1668,12 +1674,7 @@ cudaError_t configure_stream_kernels() {
   if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 3, 2, kModeSeedReq>, stream_smem<32, 3>())) != cudaSuccess) return e;
-  if ((e = opt_in(k_stream<64, 2, 4, 2, kModeNormal, __nv_bfloat16, 128>, stream_smem<64, 4, __nv_bfloat16, 128>())) !=
-      cudaSuccess)
-    return e;
-  if ((e = opt_in(k_stream<64, 1, 2, 4, kModeNormal, __nv_bfloat16, 128>, stream_smem<64, 2, __nv_bfloat16, 128>())) !=
-      cudaSuccess)
-    return e;
+
   if ((e = opt_in(k_stream<32, 1, 4, 2, kModeSeedReq, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
       cudaSuccess)
     return e;
@@ -1742,13 +1743,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     }
     if (ev0) cudaEventRecord(ev0, s);
-    if (a.trie.V <= 8192 && g_stream_variant == 4)   // 128-thread groups, 64 tokens per thread, 2 groups per CTA
-      launch_pdl(k_stream<64, 2, 4, 2, kModeNormal, bf, 128>, std::min(total, 2 * sms), 2 * 128 + 32,
-                 stream_smem<64, 4, bf, 128>(), s, a, total, 0);
-    else if (a.trie.V <= 8192 && g_stream_variant == 5)   // 128-thread groups, one per CTA, 4 CTAs per SM
-      launch_pdl(k_stream<64, 1, 2, 4, kModeNormal, bf, 128>, std::min(total, 4 * sms), 128 + 32,
-                 stream_smem<64, 2, bf, 128>(), s, a, total, 0);
-    else if (a.trie.V <= 8192)
+    if (a.trie.V <= 8192)
       launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s,
           a, total, 0);
     else   // 16384-token rows: one 512-thread consumer group per SM, 4 x 32 KB stages

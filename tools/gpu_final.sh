@@ -1,0 +1,27 @@
+#!/bin/bash
+# Round-end measurement on one B200: bench lines of every config, the default bench exactly as the
+# driver runs it, the reference arm, the ncu launch list of the default bench and one ncu --set full
+# capture of the dominant kernel per config (profiles/ncu_k_stream_*_traffic.json via
+# tools/traffic_json.py, read back on the dev box). Outputs under gpurun_out/.
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/final_smi.txt 2>&1
+run() { n=$1; shift; timeout 900 python bench.py "$@" > gpurun_out/final_$n.json 2> gpurun_out/final_$n.err; echo "bench $n rc=$?"; }
+run default
+timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/final_reference.json 2> gpurun_out/final_reference.err; echo "reference rc=$?"
+run C3s4 --sigma 4 --no-cpu-baseline --no-e2e
+run C3bf16 --logits bf16 --no-cpu-baseline --no-e2e
+run C2 --config C2 --no-cpu-baseline --no-e2e
+run C3Z --config C3Z --no-cpu-baseline --no-e2e
+run C4 --config C4 --steps 10 --no-cpu-baseline
+run C5w --config C5 --split weak --steps 10 --no-cpu-baseline --no-e2e
+run C5 --config C5 --steps 10 --no-cpu-baseline
+run heap --paper-heap --no-graph --steps 10 --no-cpu-baseline --no-e2e
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv \
+  python bench.py --profile --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/final_launches.log 2>&1; echo "launch list rc=$?"
+bash tools/ncu_traffic.sh C3_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1'
+bash tools/ncu_traffic.sh C3_f32_s4 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1' --sigma 4
+bash tools/ncu_traffic.sh C3_bf16 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?4, (\(int\))?3, (\(int\))?0, __nv_bfloat16, (\(int\))?256, (\(int\))?1' --logits bf16
+bash tools/ncu_traffic.sh C2_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1' --config C2
+bash tools/ncu_traffic.sh C4_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?2' --config C4
+bash tools/ncu_traffic.sh C5_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?8' --config C5 --split weak

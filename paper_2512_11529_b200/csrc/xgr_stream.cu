@@ -826,7 +826,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 #ifdef XGR_NO_ROT   // A/B builds only
   constexpr bool ROT = false;
 #else
-  constexpr bool ROT = EPT == 32 && sizeof(TI) == 4;
+  constexpr bool ROT = EPT == 32 && sizeof(TI) == 4 && C == 1;   // (clusters: more registers, spills)
 #endif
   extern __shared__ __align__(128) unsigned char s_dynb[];
   TI* s_row = reinterpret_cast<TI*>(s_dynb);                                         // [NS][VT]
@@ -1243,23 +1243,23 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         // delivers its partial with an asynchronous remote store that completes 8 of those bytes
         mbar_arrive_tx(&xbar[xs], 8u * C);
         const float2 mine2 = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
-#pragma unroll
+#pragma unroll 1
         for (int r = 0; r < C; ++r)
           st_async_f2(mapa(smem_u32(&mbox[xs][crank]), (uint32_t)r), mine2, mapa(smem_u32(&xbar[xs]), (uint32_t)r));
       }
       mbar_wait(&xbar[xs], (uint32_t)(xit / NXS) & 1u);
       ++xit;
-      float2 q[C];   // all C partials loaded at once (the combine is on every row's critical path)
+      // the combine is on every row's critical path: unrolled, loads issued together (the maxima
+      // first, then the pairs -- fewer live registers than holding all C pairs through both)
+      M = mbox[xs][0].x;
 #pragma unroll
-      for (int r = 0; r < C; ++r) q[r] = mbox[xs][r];
-      M = q[0].x;
-#pragma unroll
-      for (int r = 1; r < C; ++r) M = fmaxf(M, q[r].x);
+      for (int r = 1; r < C; ++r) M = fmaxf(M, mbox[xs][r].x);
       Z = 0.f;
 #pragma unroll
       for (int r = 0; r < C; ++r) {
-        if (q[r].y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q[r].y, ex2f(__fmul_rn(__fsub_rn(q[r].x, M), kLog2eS))));
-        else if (q[r].y != q[r].y) Z = q[r].y;
+        const float2 q = mbox[xs][r];
+        if (q.y > 0.f) Z = __fadd_rn(Z, __fmul_rn(q.y, ex2f(__fmul_rn(__fsub_rn(q.x, M), kLog2eS))));
+        else if (q.y != q.y) Z = q.y;
       }
     }
     if (MODE == kModeStats) {   // local (m, Z) of this rank's columns; an empty slice is (-inf, 0)

@@ -137,3 +137,18 @@ def test_c2_full_size_bf16(xgr):
     assert np.all(out["n_live"] == bw)
     cnt = bs.counters()
     assert cnt["overflow"] == 0, cnt
+
+
+@pytest.mark.parametrize("vocab,nd,n,bw,batch", [(16384, 3, 20_000_000, 256, 4), (65536, 2, 3_000_000, 32, 2)])
+def test_bf16_cluster_rows(xgr, vocab, nd, n, bw, batch):
+    """bf16 rows wider than 8192 columns: 2-CTA (V 16384, dense level-1 nodes) and 8-CTA (V 65536,
+    the root row) column-split clusters."""
+    items = make_items(n, vocab, nd, 9090 + vocab)
+    voc = O.Vocabulary(items, vocab, nd)
+    bs = _bs(xgr, voc, bw, batch, flags=2)
+    bs.mask_build(items)
+    steps = [make_logits_torch((batch, 1 if t == 0 else bw, vocab), 70 + t, 2.0).to(torch.bfloat16)
+             for t in range(nd)]
+    bs.counters()
+    run_checked(bs, voc, steps, bw, list(range(batch)))
+    assert bs.counters()["rows_read"] > 0

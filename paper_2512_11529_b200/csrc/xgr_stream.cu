@@ -1525,9 +1525,10 @@ static size_t stream_smem() {
 static int g_num_sms = 0;
 static int g_stream_variant = 0;   // XGR_STREAM_VARIANT (tuning experiments); 0 = default
 static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows per request
-static int g_seed_kernel = 2;      // XGR_SEED_KERNEL: 2 b-major streamed seed + k_seed_theta (default),
-                                   // 0 request-major seed with theta in the same kernel (as fast at C3,
-                                   // slower at C2: one CTA per request), 1 k_seed_hist + k_seed_theta
+static int g_seed_kernel = 1;      // XGR_SEED_KERNEL: 1 k_seed_hist (one CTA per seed row, the row in
+                                   // registers) + k_seed_theta (default: 1-2% faster passes at C3 / C2),
+                                   // 2 b-major streamed seed (k_stream seed mode) + k_seed_theta,
+                                   // 0 request-major seed with theta in the same kernel
 static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>

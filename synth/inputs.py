@@ -134,29 +134,31 @@ def make_items_clustered(n: int, vocab: int, nd: int, key: int, s: float = 1.0, 
     cdf /= cdf[-1]
     rng = np.random.default_rng(key & 0xFFFFFFFFFFFFFFFF)
     vm = np.uint64(vocab - 1)
-    keys_parts, have, seen = [], 0, None
-    while have < n:
-        m = min(chunk, (n - have) * 5 // 4 + 4096)
-        h = np.full(m, np.uint64(key & 0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
-        k = np.zeros(m, dtype=np.uint64)
-        for d in range(nd):
-            hp = splitmix64(h)
-            a = (hp | np.uint64(1)) & vm
-            bb = (hp >> np.uint64(32)) & vm
-            r = np.searchsorted(cdf, rng.random(m)).astype(np.uint64)
-            r = np.minimum(r, vm)
-            with np.errstate(over="ignore"):
-                t = (r * a + bb) & vm
-                h = splitmix64(h ^ (t + np.uint64(0x51ED27 + d)))
-            k = (k << np.uint64(b)) | t
-        # first occurrences, in draw order, not seen in earlier chunks
-        _, first = np.unique(k, return_index=True)
-        k = k[np.sort(first)]
-        if seen is not None:
-            k = k[~np.isin(k, seen)]
-        keys_parts.append(k)
-        seen = k if seen is None else np.concatenate([seen, k])
-        have += k.shape[0]
+    raw = np.zeros(0, dtype=np.uint64)
+    while True:
+        m = max(4096, (n * 5) // 4 if raw.shape[0] == 0 else (n - uniq.shape[0]) * 2 + 4096)
+        parts = []
+        for s0 in range(0, m, chunk):
+            mm = min(chunk, m - s0)
+            h = np.full(mm, np.uint64(key & 0xFFFFFFFFFFFFFFFF), dtype=np.uint64)
+            k = np.zeros(mm, dtype=np.uint64)
+            for d in range(nd):
+                hp = splitmix64(h)
+                a = (hp | np.uint64(1)) & vm
+                bb = (hp >> np.uint64(32)) & vm
+                r = np.minimum(np.searchsorted(cdf, rng.random(mm)).astype(np.uint64), vm)
+                with np.errstate(over="ignore"):
+                    t = (r * a + bb) & vm
+                    h = splitmix64(h ^ (t + np.uint64(0x51ED27 + d)))
+                k = (k << np.uint64(b)) | t
+            parts.append(k)
+        raw = np.concatenate([raw] + parts)
+        # first occurrences in draw order
+        _, first = np.unique(raw, return_index=True)
+        uniq = raw[np.sort(first)]
+        if uniq.shape[0] >= n:
+            break
+    keys_parts = [uniq]
     allk = np.concatenate(keys_parts)[:n]
     out = np.empty((n, nd), dtype=np.int32)
     for d in range(nd):

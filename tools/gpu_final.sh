@@ -12,16 +12,20 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/f
 run C3s4 --sigma 4 --no-cpu-baseline --no-e2e
 run C3bf16 --logits bf16 --no-cpu-baseline --no-e2e
 run C2 --config C2 --no-cpu-baseline --no-e2e
-run C3Z --config C3Z --no-cpu-baseline --no-e2e
+timeout 1500 python bench.py --config C3Z --no-cpu-baseline --no-e2e > gpurun_out/final_C3Z.json 2> gpurun_out/final_C3Z.err; echo "bench C3Z rc=$?"
 run C4 --config C4 --steps 10 --no-cpu-baseline
 run C5w --config C5 --split weak --steps 10 --no-cpu-baseline --no-e2e
 run C5 --config C5 --steps 10 --no-cpu-baseline
 run heap --paper-heap --no-graph --steps 10 --no-cpu-baseline --no-e2e
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv \
   python bench.py --profile --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/final_launches.log 2>&1; echo "launch list rc=$?"
-bash tools/ncu_traffic.sh C3_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1'
-bash tools/ncu_traffic.sh C3_f32_s4 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1' --sigma 4
-bash tools/ncu_traffic.sh C3_bf16 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?4, (\(int\))?3, (\(int\))?0, __nv_bfloat16, (\(int\))?256, (\(int\))?1' --logits bf16
-bash tools/ncu_traffic.sh C2_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?1' --config C2
-bash tools/ncu_traffic.sh C4_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?2' --config C4
-bash tools/ncu_traffic.sh C5_f32 'k_stream<(\(int\))?32, (\(int\))?1, (\(int\))?2, (\(int\))?3, (\(int\))?0, float, (\(int\))?256, (\(int\))?8' --config C5 --split weak
+R1='(\(int\))?'
+KEEP_REP=1 bash tools/ncu_traffic.sh C3_f32 "k_stream<${R1}32, ${R1}1, ${R1}2, ${R1}3, ${R1}0, float, ${R1}256, ${R1}1" C3 f32 2
+bash tools/ncu_traffic.sh C3_f32_s4 "k_stream<${R1}32, ${R1}1, ${R1}2, ${R1}3, ${R1}0, float, ${R1}256, ${R1}1" C3 f32 4 --sigma 4
+bash tools/ncu_traffic.sh C3_bf16 "k_stream<${R1}32, ${R1}1, ${R1}4, ${R1}3, ${R1}0, __nv_bfloat16, ${R1}256, ${R1}1" C3 bf16 2 --logits bf16
+bash tools/ncu_traffic.sh C2_f32 "k_stream<${R1}32, ${R1}1, ${R1}2, ${R1}3, ${R1}0, float, ${R1}256, ${R1}1" C2 f32 2 --config C2
+bash tools/ncu_traffic.sh C4_f32 "k_stream<${R1}32, ${R1}1, ${R1}2, ${R1}3, ${R1}0, float, ${R1}256, ${R1}2" C4 f32 2 --config C4
+bash tools/ncu_traffic.sh C5_f32 "k_stream<${R1}32, ${R1}1, ${R1}2, ${R1}3, ${R1}0, float, ${R1}256, ${R1}8" C5 f32 2 --config C5 --split weak
+python tools/launch_shares.py gpurun_out/final_launches.csv > gpurun_out/final/r02_launches_xgr.txt 2>&1
+rm -f gpurun_out/final_launches.csv.gz
+du -sh gpurun_out

@@ -1,12 +1,18 @@
 #!/bin/bash
 # One `ncu --set full` capture of the dominant kernel of a bench configuration (one launch, after
-# one warm-up pass): gpurun_out/ncu_<tag>.ncu-rep. Usage: tools/ncu_traffic.sh <tag> <kernel regex>
-# <bench args...>. Read back here with tools/traffic_json.py.
-tag=$1; shift; kre=$1; shift
+# one warm-up pass), summarised on the box (tools/traffic_json.py) into
+# gpurun_out/final/profiles/{ncu_k_stream_*_traffic.json, <round>_ncu_<cfg>.txt}; the report itself
+# stays in /tmp (gpurun_out/ is capped at 64 MiB) unless KEEP_REP=1.
+# Usage: tools/ncu_traffic.sh <tag> <kernel regex> <cfg> <dtype> <sigma> <bench args...>
+tag=$1; kre=$2; cfg=$3; dt=$4; sg=$5; shift 5
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
-mkdir -p gpurun_out
+mkdir -p gpurun_out/final
+rep=/tmp/ncu_$tag
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:$kre" --launch-skip 1 -c 1 -f -o gpurun_out/ncu_$tag \
+  -k "regex:$kre" --launch-skip 1 -c 1 -f -o $rep \
   python bench.py --profile --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph "$@" \
-  > gpurun_out/ncu_$tag.log 2>&1
+  > gpurun_out/final/ncu_$tag.log 2>&1
 echo "ncu $tag rc=$?"
+python tools/traffic_json.py $rep.ncu-rep $cfg $dt $sg r02 gpurun_out/final > gpurun_out/final/traffic_$tag.log 2>&1
+[ "${KEEP_REP:-0}" = "1" ] && cp $rep.ncu-rep gpurun_out/final/
+true

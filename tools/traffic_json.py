@@ -13,6 +13,7 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 rep, cfg, dtype, sigma, tag = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4]), sys.argv[5]
+OUT = sys.argv[6] if len(sys.argv) > 6 else ROOT   # on the GPU box: a directory under gpurun_out/
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, r = rows[0], rows[1], rows[2]
@@ -30,10 +31,11 @@ summary = os.path.join("profiles", f"{tag}_ncu_{cfg}_{dtype}{'' if sigma == 2.0 
 out = {"kernel": r[hdr.index("Kernel Name")][:160], "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
        "duration_ns_under_ncu": val("gpu__time_duration.sum"),
        "source": f"{summary} (ncu --set full --clock-control none, one launch after a warm-up pass)"}
-with open(os.path.join(ROOT, "profiles", bench.traffic_key(cfg, dtype, sigma)), "w") as f:
+os.makedirs(os.path.join(OUT, "profiles"), exist_ok=True)
+with open(os.path.join(OUT, "profiles", bench.traffic_key(cfg, dtype, sigma)), "w") as f:
     json.dump(out, f, indent=1)
 s = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "ncu_summary.py"), rep], capture_output=True,
                    text=True, check=True).stdout
-with open(os.path.join(ROOT, summary), "w") as f:
+with open(os.path.join(OUT, summary), "w") as f:
     f.write(f"# {rep}: bench.py --config {cfg} --logits {dtype} --sigma {sigma:g}, dominant kernel\n" + s)
 print(json.dumps(out))

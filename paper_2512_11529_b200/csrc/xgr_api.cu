@@ -56,6 +56,7 @@ struct xgr_ctx {
   int32_t** d_thist = nullptr;
   uint32_t* scratch = nullptr;     // [3][maxB]: theta, survivor count, overflow marker
   uint32_t* next_keys[2] = {nullptr, nullptr};   // per-request next-step candidates (route), by step parity
+  int32_t* dense_list = nullptr;   // [1 + maxB]: a mixed step's dense-route requests
   uint64_t* ph_lists = nullptr;    // XGR_CFG_PAPER_HEAP: [maxB][BW][K] per-beam sorted Top-K
   int32_t* ph_cnt = nullptr;       // [maxB][BW]
   uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
@@ -135,6 +136,7 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->scratch);
   cudaFree(c->ph_lists);
   cudaFree(c->ph_cnt);
+  cudaFree(c->dense_list);
   cudaFree(c->next_keys[0]);
   cudaFree(c->next_keys[1]);
   cudaFree(c->seed_hist);
@@ -242,6 +244,7 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
     e = al((void**)&x->ph_lists, nb * K * 8);
     if (e == cudaSuccess) e = al((void**)&x->ph_cnt, nb * 4);
   }
+  if (e == cudaSuccess) e = al((void**)&x->dense_list, (size_t)(x->maxB + 1) * 4);
   if (e == cudaSuccess) e = al((void**)&x->next_keys[0], (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->next_keys[1], (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
@@ -431,6 +434,7 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   if (!sparse_route && streamed && has_sparse_nodes && !ctx->ph_lists) {
     a.defer_sparse = 1;
     a.mixed = may_mix(ctx, t) ? 1 : 0;
+    if (a.mixed) a.dense_list = ctx->dense_list;
   }
   if (!sparse_route && dtype == XGR_DTYPE_BF16 && !stream_supported(ctx->V))
     return fail(XGR_ERR_UNSUPPORTED, "step: bf16 logits on a dense step need the streaming kernels (V %% 128 == 0)");

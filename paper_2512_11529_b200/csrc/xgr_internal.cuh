@@ -123,6 +123,8 @@ struct StepArgs {
   const uint32_t* next_keys_in;   // written by the previous step's commit [batch]
   uint32_t* next_keys_out;        // this step's commit [batch] (null at the last step)
   int32_t mixed;                  // 1: both routes launched this step
+  const int32_t* dense_list;      // mixed step: [0] = number of dense-route requests, then their ids
+                                  //   ascending (built on the device by k_route_list)
   int32_t defer_sparse;           // 1: k_stream leaves sparse-parent rows to k_sparse_rows
   // paper-heap baseline (XGR_CFG_PAPER_HEAP): per-beam sorted Top-K lists [batch][BW][K] and counts
   uint64_t* ph_lists;

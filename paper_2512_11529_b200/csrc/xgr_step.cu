@@ -1454,6 +1454,37 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
 }
 
 // ---------------------------------------------------------------------------------------------
+// k_route_list (mixed step): the dense-route requests (next-step candidates counted by the previous
+// commit > kSparseCap) compacted in ascending order: list[0] = count, list[1..] = request ids.
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_route_list(const __grid_constant__ StepArgs a, int32_t* list) {
+  pdl_wait();
+  __shared__ int s_w[32];
+  __shared__ int s_base;
+  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
+  if (tid == 0) s_base = 0;
+  __syncthreads();
+  for (int c0 = 0; c0 < a.batch; c0 += 1024) {
+    const int req = c0 + tid;
+    const bool dense = req < a.batch && !req_sparse(a, req);
+    const uint32_t bal = __ballot_sync(0xffffffffu, dense);
+    if (lane == 0) s_w[warp] = __popc(bal);
+    __syncthreads();
+    int off = s_base;
+    for (int w = 0; w < warp; ++w) off += s_w[w];
+    if (dense) list[1 + off + __popc(bal & ((1u << lane) - 1u))] = req;
+    __syncthreads();
+    if (tid == 0) {
+      int t = 0;
+      for (int w = 0; w < 32; ++w) t += s_w[w];
+      s_base += t;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) list[0] = s_base;
+}
+
+// ---------------------------------------------------------------------------------------------
 // k_sparse_rows: the sparse-parent rows of a dense-route step (skewed tries mix dense and sparse
 // nodes on one level). One thread per row: theta is known (seed), so the row is skipped if
 // S_b < theta, else its legal logits are gathered by label, its lse computed (stored for the exact
@@ -1848,6 +1879,9 @@ cudaError_t launch_step(const StepArgs& a, int rows, bool sparse_route, int spar
     as.sparse_cap = kSparseCap;
     if (bf16) launch_pdl(k_sparse<512, false, __nv_bfloat16>, a.batch, 512, smem, s, as);
     else launch_pdl(k_sparse<512, false>, a.batch, 512, smem, s, as);
+    ++*launches;
+    // the dense path only walks its own requests
+    launch_pdl(k_route_list, 1, 1024, 0, s, a, const_cast<int32_t*>(a.dense_list));
     ++*launches;
     if ((e = launch_stream(a, rows, s, ev0, ev1, launches)) != cudaSuccess) return e;
     const dim3 g(a.batch, (rows + 127) / 128);

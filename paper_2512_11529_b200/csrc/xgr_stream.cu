@@ -542,7 +542,12 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   __shared__ float2 part[NW];
   __shared__ float s_tau[NW];
   __shared__ uint32_t s_hist[kSeedBins];
-  const int req = blockIdx.x, r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int req = blockIdx.x;
+  const int r = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (a.dense_list) {   // a mixed step: only the dense-route requests, listed
+    if ((int)blockIdx.x >= a.dense_list[0]) return;
+    req = a.dense_list[1 + blockIdx.x];
+  }
   // The row (always in bounds: r < rows) and the beam state are loaded up front and together;
   // only the dense slot and then its bitmap depend on earlier loads.
   const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)r * a.ld;
@@ -860,6 +865,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   if (C > 1) cluster_sync_all();   // every mailbox barrier initialised before any remote arrive
   // row k of this CTA: request-major seed: row b = k of request blockIdx.x (total = rows per CTA);
   // otherwise global row w = cl + k * ncl (b-major over the batch)
+  // a mixed step streams only its dense-route requests (a.dense_list, built on the device): rows
+  // w = b * n_dense + i of request dense_list[1 + i]
+  const int ndl = (a.dense_list && !SREQ) ? a.dense_list[0] : a.batch;
+  if (a.dense_list && !SREQ) total = ndl * (total / a.batch);
   auto row_ok = [&](int k) { return SREQ ? k < total : cl + k * ncl < total; };
 
   if (tid >= NC) {
@@ -889,8 +898,9 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       m.slot = -1;
       m.lse = 0.f;
       if (w < total) {
-        m.b = SREQ ? w : w / a.batch;
-        m.req = SREQ ? (int)blockIdx.x : w - m.b * a.batch;
+        m.b = SREQ ? w : w / ndl;
+        m.req = SREQ ? (int)blockIdx.x : w - m.b * ndl;
+        if (a.dense_list && !SREQ) m.req = a.dense_list[1 + m.req];
         const int nl = a.nlive_in ? a.nlive_in[m.req] : 1;
         m.live = m.b < nl && !req_sparse(a, m.req);   // a mixed step's sparse-route requests: k_sparse
         if (m.live) {

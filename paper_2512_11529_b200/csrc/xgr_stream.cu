@@ -1527,6 +1527,223 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write its mailbox
 }
 
+// ------------------------------------------------------------------------------------------
+// k_stream2 (XGR_STREAM_VARIANT=7): rows wider than 8192 columns (fp32, V a multiple of 8192) on
+// ONE CTA each, in NCK = V / 8192 chunks of 32 KB, two passes per row. Pass 1 streams the chunks
+// from HBM (L2 evict_last) and keeps a per-thread online (m, z); the row's (M, Z), lse and the
+// upper bound S_b - ln Z_b follow from one group reduction after the last chunk. Pass 2 streams
+// the same chunks again -- from L2, the row was just read -- and emits the candidates c >= theta
+// (pass 2 of a row whose bound is below theta only releases its stages). No cluster exchange;
+// the price is a second, L2-served read of every dense row. Stage uses: pass 1 chunks 0..NCK-1,
+// then pass 2 chunks 0..NCK-1 of the same row; a row skipped before reading takes one use.
+// ------------------------------------------------------------------------------------------
+struct Desc2 {
+  int32_t req, b, kind, chunk;   // kind: 0 nothing, 1 pass-1 chunk, 2 pass-2 chunk
+  float S, th;
+};
+
+template <int NS>
+__global__ void __launch_bounds__(256 + 32, 2) k_stream2(const __grid_constant__ StepArgs a, int total) {
+  pdl_wait();
+  constexpr int GT = 256, VT = 8192, MW = VT / 32;
+  extern __shared__ __align__(128) unsigned char s_dynb2[];
+  float* s_row = reinterpret_cast<float*>(s_dynb2);                                   // [NS][VT]
+  uint32_t* s_msk = reinterpret_cast<uint32_t*>(s_dynb2 + (size_t)NS * VT * 4);       // [NS][MW]
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
+  __shared__ Desc2 desc[NS];
+  __shared__ float2 part[GT / 32];
+  const int tid = threadIdx.x;
+  const int V = a.trie.V, W = a.trie.W, BW = a.BW;
+  const int NCK = a.Vl / VT;
+  const LevelDev& L = a.trie.lv[a.level];
+  if (tid == 0) {
+    for (int s2 = 0; s2 < NS; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], GT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int ndl = a.dense_list ? a.dense_list[0] : a.batch;
+  if (a.dense_list) total = ndl * (total / a.batch);
+
+  if (tid >= GT) {
+    // ------------------------------- producer warp ---------------------------------------
+    const int lane = tid & 31;
+    const uint64_t pol_first = policy_evict_first(), pol_keep = policy_evict_last();
+    uint32_t u = 0;   // stage uses so far
+    auto use = [&](const Desc2& d, const float* src, const uint32_t* msk, bool keep) {
+      if (lane == 0) {
+        const int st = (int)(u % NS);
+        if (u >= (uint32_t)NS) mbar_wait_sleep(&empty[st], ((u / NS) - 1) & 1);
+        desc[st] = d;
+        if (src) {
+          mbar_arrive_tx(&full[st], VT * 4 + MW * 4);
+          bulk_g2s(s_row + (size_t)st * VT, src, VT * 4, &full[st], keep ? pol_keep : pol_first);
+          bulk_g2s(s_msk + (size_t)st * MW, msk, MW * 4, &full[st], pol_keep);
+        } else {
+          mbar_arrive(&full[st]);
+        }
+      }
+      ++u;
+    };
+    for (int k = 0;; ++k) {
+      const int w = blockIdx.x + k * gridDim.x;
+      if (w >= total) break;
+      int b = w / ndl, req = w - b * ndl;
+      if (a.dense_list) req = a.dense_list[1 + req];
+      // row metadata (lane 0's loads, broadcast)
+      int kind = 0, slot = -1;
+      float S = 0.f, th = -INFINITY;
+      if (lane == 0) {
+        const int nl = a.nlive_in ? a.nlive_in[req] : 1;
+        if (b < nl && !req_sparse(a, req)) {
+          uint32_t node;
+          row_state(a, req, b, S, node);
+          th = theta_value(a.theta[req]);
+          slot = L.dense_slot ? L.dense_slot[node] : -1;
+          if (S < th) {   // every candidate of the row is <= S_b < theta: skip unread
+            a.lse[(size_t)req * BW + b] = __int_as_float(0x7fc00000);
+            if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
+          } else if (slot >= 0) {
+            kind = 1;
+          }   // sparse parents: k_sparse_rows
+        }
+      }
+      kind = __shfl_sync(0xffffffffu, kind, 0);
+      slot = __shfl_sync(0xffffffffu, slot, 0);
+      S = __shfl_sync(0xffffffffu, S, 0);
+      th = __shfl_sync(0xffffffffu, th, 0);
+      if (!kind) {
+        use(Desc2{req, b, 0, 0, S, th}, nullptr, nullptr, false);
+        continue;
+      }
+      const float* row = static_cast<const float*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld;
+      const uint32_t* bm = L.bitmap + (size_t)slot * W + (a.col0 >> 5);
+      for (int c = 0; c < NCK; ++c) use(Desc2{req, b, 1, c, S, th}, row + (size_t)c * VT, bm + c * MW, true);
+      for (int c = 0; c < NCK; ++c) use(Desc2{req, b, 2, c, S, th}, row + (size_t)c * VT, bm + c * MW, false);
+    }
+    use(Desc2{0, 0, -1, 0, 0.f, 0.f}, nullptr, nullptr, false);   // end of this CTA's rows
+    return;
+  }
+
+  // ------------------------------- consumer group -----------------------------------------
+  const int lt = tid, lane = tid & 31;
+  float tm = -INFINITY, tz = 0.f;   // this thread's running (m, z) over the row's chunks
+  float lse = 0.f, M = -INFINITY;
+  bool emit = false;
+  for (uint32_t u = 0;; ++u) {
+    // the consumer walks the same stage uses; the producer marks the end with a use of kind -1
+    const int st = (int)(u % NS);
+    mbar_wait_sleep(&full[st], (u / NS) & 1);
+    const Desc2 d = desc[st];
+    if (d.kind <= 0 || (d.kind == 2 && !emit)) {   // nothing to do with this stage
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+      if (d.kind < 0) break;
+      continue;
+    }
+    const float* srow = s_row + (size_t)st * VT + 32 * lt;
+    const uint32_t w = s_msk[(size_t)st * MW + lt];
+    const uint32_t wrot = __funnelshift_r(w, w, 4 * (lt & 7));
+    float x[32];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 raw = *reinterpret_cast<const float4*>(srow + 4 * ((i + lt) & 7));
+      const uint32_t nb = wrot >> (4 * i);
+      x[4 * i + 0] = (nb & 1u) ? raw.x : -INFINITY;
+      x[4 * i + 1] = (nb & 2u) ? raw.y : -INFINITY;
+      x[4 * i + 2] = (nb & 4u) ? raw.z : -INFINITY;
+      x[4 * i + 3] = (nb & 8u) ? raw.w : -INFINITY;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    float cm = -INFINITY;
+#pragma unroll
+    for (int e = 0; e < 32; e += 4) cm = fmaxf(cm, fmaxf(fmaxf(x[e], x[e + 1]), fmaxf(x[e + 2], x[e + 3])));
+    if (d.kind == 1) {
+      // pass 1: online (m, z) of this thread's tokens
+      if (d.chunk == 0) {
+        tm = -INFINITY;
+        tz = 0.f;
+      }
+      const float mn = fmaxf(tm, cm);
+      if (mn > -INFINITY) {
+        const float c2 = -__fmul_rn(mn, kLog2eS);
+        float2 z0 = make_float2(0.f, 0.f), z1 = make_float2(0.f, 0.f);
+        const float2 l2e = make_float2(kLog2eS, kLog2eS), cc = make_float2(c2, c2);
+#pragma unroll
+        for (int e = 0; e < 32; e += 4) {
+          const float2 a0 = __ffma2_rn(make_float2(x[e], x[e + 1]), l2e, cc);
+          const float2 a1 = __ffma2_rn(make_float2(x[e + 2], x[e + 3]), l2e, cc);
+          z0 = __fadd2_rn(z0, make_float2(ex2f(a0.x), ex2f(a0.y)));
+          z1 = __fadd2_rn(z1, make_float2(ex2f(a1.x), ex2f(a1.y)));
+        }
+        const float2 zz = __fadd2_rn(z0, z1);
+        const float sc = tm > -INFINITY ? ex2f(__fmul_rn(__fsub_rn(tm, mn), kLog2eS)) : 0.f;
+        tz = __fadd_rn(__fmul_rn(tz, sc), zz.x + zz.y);
+        tm = mn;
+      }
+      if (d.chunk == NCK - 1) {
+        // the row's (M, Z): warp combine of the threads' (m, z), then the group's warps
+        const float mw = wmax(tm);
+        float zw = (tm > -INFINITY) ? __fmul_rn(tz, ex2f(__fmul_rn(__fsub_rn(tm, mw), kLog2eS))) : 0.f;
+        zw = wsum(zw);
+        if (lane == 0) part[lt >> 5] = make_float2(mw, zw);
+        named_sync(1, GT);
+        const float2 pr = lane < GT / 32 ? part[lane] : make_float2(-INFINITY, 0.f);
+        M = wmax(pr.x);
+        float zi = (pr.x > -INFINITY) ? pr.y * ex2f(__fmul_rn(__fsub_rn(pr.x, M), kLog2eS)) : 0.f;
+        if (lane >= GT / 32) zi = 0.f;
+#pragma unroll
+        for (int o = GT / 64; o > 0; o >>= 1) zi += __shfl_xor_sync(0xffffffffu, zi, o);
+        const float Z = __shfl_sync(0xffffffffu, zi, 0);
+        named_sync(1, GT);   // part is rewritten by the next row
+        const bool finite = (Z > 0.5f) && (Z <= 3.0e38f);
+        lse = row_lse(M, Z);
+        if (lt == 0) {
+          a.lse[(size_t)d.req * BW + d.b] = finite ? lse : __int_as_float(0x7fc00000);
+          if (!finite) atomicOr(a.flags + d.req, kFlagNonfinite);
+          if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
+        }
+        emit = finite && cand_score(d.S, M, lse) >= d.th;
+        if (finite && !emit && lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
+      }
+      continue;
+    }
+    // pass 2: candidates of this chunk (rows whose bound is below theta never get here)
+    uint32_t mine = 0u;
+    if (d.th > -INFINITY) {
+      const float xthr = (d.th - d.S) + lse - 1e-5f * (fabsf(d.th) + fabsf(d.S) + 2.0f * fabsf(lse));
+      if (cm >= xthr) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (x[e] >= xthr && cand_score(d.S, x[e], lse) >= d.th) mine |= 1u << e;
+      }
+    } else {
+      mine = wrot;   // no bound: every legal token
+    }
+    const int ns = __popc(mine);
+    if (__any_sync(0xffffffffu, ns > 0)) {
+      uint32_t pos = warp_reserve((uint32_t)ns, a.surv_count + d.req);
+      uint64_t* sbuf = a.surv + (size_t)d.req * a.cap;
+      const uint32_t fbase = (uint32_t)d.b * (uint32_t)V + (uint32_t)a.col0 + (uint32_t)d.chunk * VT;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        if ((mine >> e) & 1u) {
+          const uint32_t v = 32u * lt + 4u * (uint32_t)(((e >> 2) + lt) & 7) + (uint32_t)(e & 3);
+          if (pos < (uint32_t)a.cap) sbuf[pos] = make_key(cand_score(d.S, x[e], lse), fbase + v);
+          ++pos;
+        }
+      }
+      if (a.counters_on) {
+        const int tot = __reduce_add_sync(0xffffffffu, ns);
+        if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
+      }
+    }
+  }
+}
+
 template <int EPT, int NS, typename TI = float, int GT = 256>
 static size_t stream_smem() {
   return (size_t)NS * (GT * EPT * sizeof(TI) + GT * EPT / 8);
@@ -1621,6 +1838,28 @@ static cudaError_t configure_cluster() {
   return cudaSuccess;
 }
 
+static int g_ncta2 = 0;   // resident CTAs of k_stream2 (XGR_STREAM_VARIANT=7)
+
+// XGR_STREAM_VARIANT=7: rows of V = NCK x 8192 fp32 columns on one CTA each, two passes (k_stream2);
+// the theta seed is the cluster kernel's seed pass.
+template <int C>
+static void launch_stream2(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
+                           int* launches) {
+  const int total = a.batch * rows;
+  const int r0 = std::min(a.theta_rows, rows);
+  if (r0 > 0) {
+    const int ns = a.batch * r0;
+    const int ncl = std::min(g_ncl[0][1][C], ns);
+    launch_cl(k_stream<32, 1, 2, 3, kModeSeedHist, float, 256, C>, C * ncl, 288, stream_smem<32, 2>(), s, C, a, ns, 0);
+    ++*launches;
+  }
+  launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
+  if (ev0) cudaEventRecord(ev0, s);
+  launch_pdl(k_stream2<3>, std::min(total, g_ncta2), 288, (size_t)3 * (8192 * 4 + 1024), s, a, total);
+  if (ev1) cudaEventRecord(ev1, s);
+  *launches += 2;
+}
+
 // Dense step of a row wider than 8192 columns on one GPU: clusters of C CTAs, 8192 columns or fewer
 // each (V % (128 C) == 0): histogram seed over R0 rows, theta, the streamed pass.
 template <int C>
@@ -1693,6 +1932,13 @@ cudaError_t configure_stream_kernels() {
       cudaSuccess)
     return e;
   if ((e = configure_cluster<2>()) || (e = configure_cluster<4>()) || (e = configure_cluster<8>())) return e;
+  {
+    const size_t sm2 = (size_t)3 * (8192 * 4 + 1024);
+    if ((e = opt_in(k_stream2<3>, sm2))) return e;
+    int per = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream2<3>, 288, sm2))) return e;
+    g_ncta2 = std::max(1, per) * (g_num_sms > 0 ? g_num_sms : 148);
+  }
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
 
@@ -1727,6 +1973,14 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
   const int C = cluster_of(a.Vl);
+  if (C > 1 && g_stream_variant == 7 && a.dtype == XGR_DTYPE_F32 && !a.topk && a.Vl % 8192 == 0) {
+    switch (C) {
+      case 2: launch_stream2<2>(a, rows, s, ev0, ev1, launches); break;
+      case 4: launch_stream2<4>(a, rows, s, ev0, ev1, launches); break;
+      default: launch_stream2<8>(a, rows, s, ev0, ev1, launches); break;
+    }
+    return cudaGetLastError();
+  }
   if (C > 2 || (C == 2 && !a.topk && g_stream_variant != 3)) {   // rows wider than 8192: column-split clusters
     switch (C) {
       case 2: launch_stream_cluster<2>(a, rows, s, ev0, ev1, launches); break;

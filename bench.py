@@ -706,10 +706,17 @@ def main(argv=None):
         print(json.dumps(run_reference(args, cfg)), flush=True)
         return 0
     if world > 1:
+        # NCCL's communicator lines (rank count, transport) on stderr, so a multi-GPU run's log
+        # shows the communicator the timings came from; stdout keeps the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist.barrier(device_ids=[local_rank])   # creates the communicator now (its INIT lines)
+        print(f"[bench] rank {rank} of {world}: NCCL communicator on cuda:{local_rank}", file=sys.stderr, flush=True)
     res = run_ours(args, cfg, rank, world, local_rank)
     if rank == 0:
         print(json.dumps(res), flush=True)

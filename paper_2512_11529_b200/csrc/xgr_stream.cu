@@ -1528,7 +1528,8 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 }
 
 // ------------------------------------------------------------------------------------------
-// k_stream2 (XGR_STREAM_VARIANT=7): rows wider than 8192 columns (fp32, V a multiple of 8192) on
+// k_stream2 (default for V >= 32768 fp32; XGR_STREAM_VARIANT=7 also for V = 16384): rows wider than
+// 8192 columns (fp32, V a multiple of 8192) on
 // ONE CTA each, in NCK = V / 8192 chunks of 32 KB, two passes per row. Pass 1 streams the chunks
 // from HBM (L2 evict_last) and keeps a per-thread online (m, z); the row's (M, Z), lse and the
 // upper bound S_b - ln Z_b follow from one group reduction after the last chunk. Pass 2 streams
@@ -1840,8 +1841,8 @@ static cudaError_t configure_cluster() {
 
 static int g_ncta2 = 0;   // resident CTAs of k_stream2 (XGR_STREAM_VARIANT=7)
 
-// XGR_STREAM_VARIANT=7: rows of V = NCK x 8192 fp32 columns on one CTA each, two passes (k_stream2);
-// the theta seed is the cluster kernel's seed pass.
+// Rows of V = NCK x 8192 fp32 columns on one CTA each, two passes (k_stream2; the default for
+// NCK >= 4); the theta seed is the cluster kernel's seed pass.
 template <int C>
 static void launch_stream2(const StepArgs& a, int rows, cudaStream_t s, cudaEvent_t ev0, cudaEvent_t ev1,
                            int* launches) {
@@ -1973,7 +1974,12 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   const int sms = g_num_sms > 0 ? g_num_sms : 148;
   const int grid = std::min(total, sms);
   const int C = cluster_of(a.Vl);
-  if (C > 1 && g_stream_variant == 7 && a.dtype == XGR_DTYPE_F32 && !a.topk && a.Vl % 8192 == 0) {
+  // fp32 rows of 4+ x 8192 columns: one CTA per row in two passes (k_stream2; C5 one context 3.34 vs
+  // 4.72 ms with 8-CTA clusters); 2 x 8192 (C4) keeps the 2-CTA clusters (3.55 vs 4.31 ms).
+  // XGR_STREAM_VARIANT=7 forces k_stream2, 8 forces the clusters.
+  const bool two_pass = a.dtype == XGR_DTYPE_F32 && !a.topk && a.Vl % 8192 == 0 &&
+                        ((C >= 4 && g_stream_variant != 8) || (C > 1 && g_stream_variant == 7));
+  if (C > 1 && two_pass) {
     switch (C) {
       case 2: launch_stream2<2>(a, rows, s, ev0, ev1, launches); break;
       case 4: launch_stream2<4>(a, rows, s, ev0, ev1, launches); break;

@@ -1814,7 +1814,6 @@ static int max_clusters(K k, int block, size_t smem, int C) {
 
 // the column-split (cluster) streaming kernels: normal and seed pass, fp32 and bf16
 static int g_ncl[2][2][9];   // [dtype bf16][seed mode][C]: clusters per launch
-static int g_ncl_512[9];     // clusters of the 512-thread-group kernel (XGR_STREAM_VARIANT=6)
 
 template <int C>
 static cudaError_t configure_cluster() {
@@ -1830,12 +1829,6 @@ static cudaError_t configure_cluster() {
   g_ncl[0][1][C] = max_clusters(ks, 288, sf, C);
   g_ncl[1][0][C] = max_clusters(bn, 288, sb, C);
   g_ncl[1][1][C] = max_clusters(bsd, 288, sb, C);
-  if constexpr (C == 2 || C == 4) {
-    auto k5 = k_stream<32, 1, 3, 1, kModeNormal, float, 512, C>;
-    const size_t s5 = stream_smem<32, 3, float, 512>();
-    if ((e = opt_in(k5, s5))) return e;
-    g_ncl_512[C] = max_clusters(k5, 544, s5, C);
-  }
   return cudaSuccess;
 }
 
@@ -1880,17 +1873,6 @@ static void launch_stream_cluster(const StepArgs& a, int rows, cudaStream_t s, c
   launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
   if (ev0) cudaEventRecord(ev0, s);
   const int ncl = std::min(g_ncl[b16][0][C], total);
-  if constexpr (C >= 4) {
-    if (!b16 && g_stream_variant == 6) {   // half as many CTAs per row: 512-thread groups, 16384 columns each
-      constexpr int C2 = C / 2;
-      const int n2 = std::min(g_ncl_512[C2], total);
-      launch_cl(k_stream<32, 1, 3, 1, kModeNormal, float, 512, C2>, C2 * n2, 544, stream_smem<32, 3, float, 512>(), s,
-                C2, a, total, 0);
-      if (ev1) cudaEventRecord(ev1, s);
-      *launches += 2;
-      return;
-    }
-  }
   if (b16) launch_cl(k_stream<32, 1, 4, 3, kModeNormal, bf, 256, C>, C * ncl, 288, stream_smem<32, 4, bf>(), s, C, a, total, 0);
   else launch_cl(k_stream<32, 1, 2, 3, kModeNormal, float, 256, C>, C * ncl, 288, stream_smem<32, 2>(), s, C, a, total, 0);
   if (ev1) cudaEventRecord(ev1, s);

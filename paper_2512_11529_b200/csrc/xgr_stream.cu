@@ -1544,7 +1544,7 @@ struct Desc2 {
 };
 
 template <int NS>
-__global__ void __launch_bounds__(256 + 32, NS == 2 ? 3 : 2) k_stream2(const __grid_constant__ StepArgs a, int total) {
+__global__ void __launch_bounds__(256 + 32, 2) k_stream2(const __grid_constant__ StepArgs a, int total) {
   pdl_wait();
   constexpr int GT = 256, VT = 8192, MW = VT / 32;
   extern __shared__ __align__(128) unsigned char s_dynb2[];
@@ -1832,7 +1832,7 @@ static cudaError_t configure_cluster() {
   return cudaSuccess;
 }
 
-static int g_ncta2 = 0, g_ncta2b = 0;   // resident CTAs of k_stream2<3> / k_stream2<2>
+static int g_ncta2 = 0;   // resident CTAs of k_stream2 (XGR_STREAM_VARIANT=7)
 
 // Rows of V = NCK x 8192 fp32 columns on one CTA each, two passes (k_stream2; the default for
 // NCK >= 4); the theta seed is the cluster kernel's seed pass.
@@ -1849,10 +1849,7 @@ static void launch_stream2(const StepArgs& a, int rows, cudaStream_t s, cudaEven
   }
   launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
   if (ev0) cudaEventRecord(ev0, s);
-  if (g_stream_variant == 9)   // A/B: 2 stages, 3 CTAs per SM
-    launch_pdl(k_stream2<2>, std::min(total, g_ncta2b), 288, (size_t)2 * (8192 * 4 + 1024), s, a, total);
-  else
-    launch_pdl(k_stream2<3>, std::min(total, g_ncta2), 288, (size_t)3 * (8192 * 4 + 1024), s, a, total);
+  launch_pdl(k_stream2<3>, std::min(total, g_ncta2), 288, (size_t)3 * (8192 * 4 + 1024), s, a, total);
   if (ev1) cudaEventRecord(ev1, s);
   *launches += 2;
 }
@@ -1924,10 +1921,6 @@ cudaError_t configure_stream_kernels() {
     int per = 0;
     if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream2<3>, 288, sm2))) return e;
     g_ncta2 = std::max(1, per) * (g_num_sms > 0 ? g_num_sms : 148);
-    const size_t sm2b = (size_t)2 * (8192 * 4 + 1024);
-    if ((e = opt_in(k_stream2<2>, sm2b))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_stream2<2>, 288, sm2b))) return e;
-    g_ncta2b = std::max(1, per) * (g_num_sms > 0 ? g_num_sms : 148);
   }
   return opt_in(k_seed<512, 2>, stream_smem<64, 2>());
 }
@@ -1967,7 +1960,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   // 4.72 ms with 8-CTA clusters); 2 x 8192 (C4) keeps the 2-CTA clusters (3.55 vs 4.31 ms).
   // XGR_STREAM_VARIANT=7 forces k_stream2, 8 forces the clusters.
   const bool two_pass = a.dtype == XGR_DTYPE_F32 && !a.topk && a.Vl % 8192 == 0 &&
-                        ((C >= 4 && g_stream_variant != 8) || (C > 1 && (g_stream_variant == 7 || g_stream_variant == 9)));
+                        ((C >= 4 && g_stream_variant != 8) || (C > 1 && g_stream_variant == 7));
   if (C > 1 && two_pass) {
     switch (C) {
       case 2: launch_stream2<2>(a, rows, s, ev0, ev1, launches); break;

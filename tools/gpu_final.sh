@@ -15,6 +15,7 @@ run C2 --config C2 --no-cpu-baseline --no-e2e
 timeout 1500 python bench.py --config C3Z --no-cpu-baseline --no-e2e > gpurun_out/final_C3Z.json 2> gpurun_out/final_C3Z.err; echo "bench C3Z rc=$?"
 run C4 --config C4 --steps 10 --no-cpu-baseline
 run C5w --config C5 --split weak --steps 10 --no-cpu-baseline --no-e2e
+run C3Zb --config C3Z --no-cpu-baseline --no-e2e --steps 10
 run C5 --config C5 --steps 10 --no-cpu-baseline
 run heap --paper-heap --no-graph --steps 10 --no-cpu-baseline --no-e2e
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches.csv \

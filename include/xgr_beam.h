@@ -77,7 +77,8 @@ typedef struct {
   int32_t nd;         /* ND: tokens per item (trie depth), 1..8; nd*ceil(log2 V) <= 64    */
   int32_t beam_width; /* BW, 1..1024                                                      */
   int32_t top_k;      /* per-beam K: each beam keeps its K best candidates
-                         (score desc, token asc) before the global Top-BW. 0 or >= BW: none */
+                         (score desc, token asc) before the global Top-BW. 0 or >= BW: none.
+                         0 < K < BW needs V <= 16384 and nranks == 1 (else UNSUPPORTED)    */
   int32_t max_batch;  /* max requests per step call, >= 1                                 */
   int32_t device;     /* CUDA device ordinal                                             */
   int32_t nranks;     /* codebook shards G >= 1 (1: no shard). G > 1: V % G == 0 and       */
@@ -111,6 +112,12 @@ xgr_status xgr_mask_build(xgr_ctx* ctx, const int32_t* items, int64_t n_items, v
  *   Rows >= n_live and columns outside the legal set are never read. 16-byte aligned, ld % 4 == 0,
  *   ld >= V. At t = 1 rows >= 1 (only row 0 is read); at t > 1 rows >= BW.
  * batch: 1..max_batch, fixed by the first step of a batch.
+ * Route (no effect on results): a step whose requests' legal candidates fit on chip (rows x max
+ * children of the level <= 16384) runs the sparse kernel; otherwise the dense streaming path --
+ * one CTA per row up to 8192 columns, 2-CTA thread-block clusters for 16384, one CTA per row in
+ * two passes for 32768 and 65536 (V % (128 C) == 0 for C = V/8192 rounded up to a power of two;
+ * other V > 16384 return XGR_ERR_UNSUPPORTED on a dense step). A level that mixes dense and sparse
+ * nodes takes both routes, per request (the previous step's commit counted its candidates).
  * Enqueues only (no sync, no allocation); graph-capturable. */
 xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32_t rows,
                          int64_t ld, void* stream);
@@ -122,9 +129,9 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
 /* xgr_beam_step with the logits' element type given (PAPER.md L361, L376
  * leave the dtype open). XGR_DTYPE_BF16: DEVICE bf16 [batch][rows][ld], 16-byte aligned rows
  * (ld % 8 == 0); every value is widened exactly to fp32 and the step computes in fp32 as for
- * XGR_DTYPE_F32 (the oracle widens the same values). bf16 needs V % 128 == 0 and V <= 16384 for
- * dense steps (the streaming kernels); otherwise XGR_ERR_UNSUPPORTED, as for any other dtype or
- * a sharded ctx. XGR_DTYPE_F32 is exactly xgr_beam_step. */
+ * XGR_DTYPE_F32 (the oracle widens the same values). bf16 dense steps need the streaming kernels
+ * (V % 128 == 0; V > 8192 in column-split clusters); otherwise XGR_ERR_UNSUPPORTED, as for any
+ * other dtype or a sharded ctx. XGR_DTYPE_F32 is exactly xgr_beam_step. */
 xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype,
                             int32_t rows, int64_t ld, void* stream);
 

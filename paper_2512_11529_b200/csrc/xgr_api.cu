@@ -60,6 +60,7 @@ struct xgr_ctx {
   uint64_t* ph_lists = nullptr;    // XGR_CFG_PAPER_HEAP: [maxB][BW][K] per-beam sorted Top-K
   int32_t* ph_cnt = nullptr;       // [maxB][BW]
   uint32_t* seed_hist = nullptr;   // [maxB][kSeedBins]
+  uint32_t* seed_cnt = nullptr;    // [maxB]
   float* head_logits = nullptr;    // [maxB][kSparseCap]: legal logits of a fused-head sparse step
   uint64_t* surv = nullptr;        // [maxB][cap]
   float* lse = nullptr;            // [maxB][BW]
@@ -140,6 +141,7 @@ static void ctx_free(xgr_ctx* c) {
   cudaFree(c->next_keys[0]);
   cudaFree(c->next_keys[1]);
   cudaFree(c->seed_hist);
+  cudaFree(c->seed_cnt);
   cudaFree(c->head_logits);
   cudaFree(c->surv);
   cudaFree(c->lse);
@@ -250,6 +252,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (e == cudaSuccess) e = al((void**)&x->seed_hist, (size_t)x->maxB * kSeedBins * 4);
   if (e == cudaSuccess) e = al((void**)&x->head_logits, (size_t)x->maxB * kSparseCap * 4);
   if (e == cudaSuccess) e = cudaMemset(x->seed_hist, 0, (size_t)x->maxB * kSeedBins * 4);
+  if (e == cudaSuccess) e = al((void**)&x->seed_cnt, (size_t)x->maxB * 4);
+  if (e == cudaSuccess) e = cudaMemset(x->seed_cnt, 0, (size_t)x->maxB * 4);
   if (e == cudaSuccess) e = al((void**)&x->surv, (size_t)x->maxB * x->cap * 8);
   if (e == cudaSuccess) e = al((void**)&x->lse, nb * 4);
   if (e == cudaSuccess) e = al((void**)&x->flags, (size_t)x->maxB * 4);
@@ -383,6 +387,7 @@ static xgr_status step_args(xgr_ctx* ctx, int32_t batch, const void* logits, int
   a.surv_count = ctx->scratch + ctx->maxB;
   a.ovf = ctx->scratch + 2 * ctx->maxB;
   a.seed_hist = ctx->seed_hist;
+  a.seed_cnt = ctx->seed_cnt;
   a.surv = ctx->surv;
   a.lse = ctx->lse;
   a.flags = ctx->flags;

@@ -112,6 +112,7 @@ struct StepArgs {
   uint32_t* surv_count;
   uint32_t* ovf;        // this step's overflow marker
   uint32_t* seed_hist;  // [batch][kSeedBins] histogram of S_0 - c over the seed rows (zero between steps)
+  uint32_t* seed_cnt;   // [batch] seed CTAs finished this step (XGR_SEED_KERNEL=3; zero between steps)
   uint64_t* surv;       // [batch][cap] survivor keys
   float* lse;           // [batch][BW] per-row lse (NaN: row not read)
   uint32_t* flags;      // sticky per-request status bits

@@ -533,9 +533,7 @@ __global__ void __launch_bounds__(CTR * R0, 1) k_seed(const __grid_constant__ St
 // <= the request's BW-th best score. The seed rows are then streamed like any other row.
 // ------------------------------------------------------------------------------------------
 template <int T, int NCH, typename TI = float>
-__global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
-  pdl_wait();
-  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
+__device__ __forceinline__ void seed_hist_row(const StepArgs& a) {
   constexpr int CH = 16 / (int)sizeof(TI);   // tokens per 16-byte chunk
   constexpr int VPT = NCH * CH / 4;          // x[] holds 4 * VPT = NCH * CH tokens per thread
   constexpr int NW = T / 32;
@@ -716,19 +714,25 @@ __global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArg
   }
 }
 
-template <int T>
-__global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepArgs a) {
+template <int T, int NCH, typename TI = float>
+__global__ void __launch_bounds__(T) k_seed_hist(const __grid_constant__ StepArgs a) {
   pdl_wait();
   if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
+  seed_hist_row<T, NCH, TI>(a);
+}
+
+// theta of request req from its histogram (one CTA of T threads; see k_seed_theta)
+template <int T>
+__device__ __forceinline__ void seed_theta_req(const StepArgs& a, int req) {
   constexpr int PER = kSeedBins / T;
   __shared__ uint32_t s_w[T / 32];
   __shared__ int s_bin;
-  const int req = blockIdx.x, tid = threadIdx.x, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
   uint32_t* h = a.seed_hist + (size_t)req * kSeedBins;
   uint32_t c[PER], loc = 0;
 #pragma unroll
   for (int j = 0; j < PER; ++j) {
-    c[j] = h[tid * PER + j];
+    c[j] = __ldcg(h + tid * PER + j);   // the seed CTAs' atomics live in L2
     loc += c[j];
   }
 #pragma unroll
@@ -766,6 +770,38 @@ __global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepAr
     a.surv_count[req] = 0u;
     a.ovf[req] = 0u;
   }
+}
+
+template <int T>
+__global__ void __launch_bounds__(T) k_seed_theta(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  if (a.dbg & (1 << 20)) pdl_trigger();   // early trigger only on request (XGR_DEBUG_FLAGS bit 20)
+  seed_theta_req<T>(a, blockIdx.x);
+}
+
+// The seed and theta in one kernel (XGR_SEED_KERNEL=3): the last of a request's R0 seed CTAs to
+// finish (per-request arrival counter, fenced) derives theta from the completed histogram.
+template <int T, int NCH, typename TI = float>
+__global__ void __launch_bounds__(T) k_seed_hist_theta(const __grid_constant__ StepArgs a) {
+  pdl_wait();
+  __shared__ int s_last;
+  seed_hist_row<T, NCH, TI>(a);
+  int req = blockIdx.x;
+  if (a.dense_list) {
+    if ((int)blockIdx.x >= a.dense_list[0]) return;
+    req = a.dense_list[1 + blockIdx.x];
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const uint32_t prev = atomicAdd(a.seed_cnt + req, 1u);
+    s_last = prev == gridDim.y - 1;
+    if (s_last) a.seed_cnt[req] = 0u;   // ready for the next dense step
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  seed_theta_req<T>(a, req);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -2008,6 +2044,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
   }
   if (a.trie.V <= 8192) {
     int seeded = g_seed_rows == 2 ? 2 : 4;
+    bool fused_theta = false;
     if ((g_seed_mode >= 1 && g_seed_kernel == 0) && !a.topk) {
       // histogram seed over rows 0..R0-1, one CTA per request, theta in the same kernel; every row
       // is then streamed
@@ -2018,7 +2055,10 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
     } else if (g_seed_mode >= 1 || a.topk) {   // histogram seed over rows 0..R0-1; every row is then streamed
       const int r0 = std::min(a.theta_rows, rows);
       if (r0 > 0) {
-        if (g_seed_kernel == 1 || a.topk) {   // one CTA per seed row (XGR_SEED_KERNEL=1; Top-K cap)
+        if (g_seed_kernel == 3 && !a.topk) {   // seed + theta in one kernel (A/B)
+          launch_pdl(k_seed_hist_theta<256, 8>, dim3(a.batch, r0), 256, 0, s, a);
+          fused_theta = true;
+        } else if (g_seed_kernel == 1 || a.topk) {   // one CTA per seed row (XGR_SEED_KERNEL=1; Top-K cap)
           launch_pdl(k_seed_hist<256, 8>, dim3(a.batch, r0), 256, 0, s, a);
         } else {                    // the seed rows streamed by the persistent kernel
           const int ns = a.batch * r0;
@@ -2026,7 +2066,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
         }
         ++*launches;
       }
-      launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
+      if (!fused_theta) launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
       seeded = 0;
     } else if (seeded == 2) {
       launch_pdl(k_seed<256, 2>, a.batch, 512, stream_smem<32, 2>(), s, a);

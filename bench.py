@@ -194,16 +194,19 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0}, "fallback"
 
 
-def traffic_key(cfg_name: str, dtype: str, sigma: float) -> str:
+def traffic_key(cfg_name: str, dtype: str, sigma: float, split: str = "") -> str:
+    """split: "" for the config's default partition, else its name (e.g. C5 with --split weak)."""
     s = "" if sigma == 2.0 else f"_s{sigma:g}"
-    return f"ncu_k_stream_{cfg_name}_{dtype}{s}_traffic.json"
+    sp = f"_{split}" if split else ""
+    return f"ncu_k_stream_{cfg_name}{sp}_{dtype}{s}_traffic.json"
 
 
-def committed_traffic(cfg_name: str, dtype: str = "f32", sigma: float = 2.0):
+def committed_traffic(cfg_name: str, dtype: str = "f32", sigma: float = 2.0, split: str = ""):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full summary of
-    THIS config / dtype / sigma (profiles/ncu_k_stream_<cfg>_<dtype>[_s<sigma>]_traffic.json), or
-    None when no capture of it is committed."""
-    p = os.path.join(ROOT, "profiles", traffic_key(cfg_name, dtype, sigma))
+    THIS config / partition / dtype / sigma
+    (profiles/ncu_k_stream_<cfg>[_<split>]_<dtype>[_s<sigma>]_traffic.json), or None when no
+    capture of it is committed."""
+    p = os.path.join(ROOT, "profiles", traffic_key(cfg_name, dtype, sigma, split))
     try:
         with open(p) as f:
             d = json.load(f)
@@ -530,9 +533,16 @@ def account(args, cfg, plan, dev, items, logits, main_ms, dense_steps, per_step,
         mean_ms = sum(main_ms) / len(main_ms)
         achieved = algb["alg_bytes"] / (mean_ms / 1e3) / 1e9
         step_dense = statistics.median(per_step[dense_steps[0] - 1]) if dense_steps else None
-        tr = committed_traffic(cfg["name"], args.logits, args.sigma)
-        kname = ("k_stream stats mode (codebook shard: per-row (m, Z) over each shard's columns; every local shard)"
-                 if shard else "k_stream (dense step: TMA row stream, masked log-softmax, score add, pruned emit)")
+        tr = committed_traffic(cfg["name"], args.logits, args.sigma,
+                               "" if args.split in ("auto", split_mode(cfg)) else args.split)
+        if shard:
+            kname = "k_stream stats mode (codebook shard: per-row (m, Z) over each shard's columns; every local shard)"
+        elif cfg["vocab"] >= 32768 and args.logits == "f32":
+            kname = "k_stream2 (dense step, one CTA per row in two passes: online softmax, then emission from L2)"
+        elif cfg["vocab"] > 8192:
+            kname = "k_stream, 2-CTA column-split clusters (dense step)"
+        else:
+            kname = "k_stream (dense step: TMA row stream, masked log-softmax, score add, pruned emit)"
         out["roofline"] = {
             "bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

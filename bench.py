@@ -535,7 +535,10 @@ def account(args, cfg, plan, dev, items, logits, main_ms, dense_steps, per_step,
         step_dense = statistics.median(per_step[dense_steps[0] - 1]) if dense_steps else None
         tr = committed_traffic(cfg["name"], args.logits, args.sigma,
                                "" if args.split in ("auto", split_mode(cfg)) else args.split)
-        if shard:
+        if args.paper_heap:
+            tr = None   # no ncu capture of the baseline's kernels is committed
+            kname = "k_ph_rows (the paper's per-beam Top-K lists; baseline, XGR_CFG_PAPER_HEAP)"
+        elif shard:
             kname = "k_stream stats mode (codebook shard: per-row (m, Z) over each shard's columns; every local shard)"
         elif cfg["vocab"] >= 32768 and args.logits == "f32":
             kname = "k_stream2 (dense step, one CTA per row in two passes: online softmax, then emission from L2)"
@@ -547,7 +550,8 @@ def account(args, cfg, plan, dev, items, logits, main_ms, dense_steps, per_step,
             "bound": "hbm", "kernel": kname,
             "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
             "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src == "measured" else "fallback 6.65 TB/s",
-            "traffic": (tr or {}).get("dram_bytes_per_launch"),
+            # the shard line's stats pass is SHARDS launches (one per local shard ctx); the capture is one of them
+            "traffic": ((tr or {}).get("dram_bytes_per_launch") or 0) * (SHARDS if shard else 1) or None,
             "traffic_source": (tr or {}).get("source"),
             "traffic_file": (tr or {}).get("file"),
             "alg_bytes_per_launch": algb["alg_bytes"], "full_bytes_per_launch": algb["full_bytes"],

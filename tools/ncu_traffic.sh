@@ -3,6 +3,7 @@
 # one warm-up pass), summarised on the box (tools/traffic_json.py) into
 # gpurun_out/final/profiles/{ncu_k_stream_*_traffic.json, <round>_ncu_<cfg>.txt}; the report itself
 # stays in /tmp (gpurun_out/ is capped at 64 MiB) unless KEEP_REP=1.
+# LSKIP=<n>: matching launches to skip (default 1: the warm-up pass's first).
 # Usage: tools/ncu_traffic.sh <tag> <kernel regex> <cfg> <dtype> <sigma> <split|-> <bench args...>
 tag=$1; kre=$2; cfg=$3; dt=$4; sg=$5; sp=$6; shift 6
 [ "$sp" = "-" ] && sp=""
@@ -10,7 +11,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out/final
 rep=/tmp/ncu_$tag
 timeout 1200 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k "regex:$kre" --launch-skip 1 -c 1 -f -o $rep \
+  -k "regex:$kre" --launch-skip ${LSKIP:-1} -c 1 -f -o $rep \
   python bench.py --profile --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-graph "$@" \
   > gpurun_out/final/ncu_$tag.log 2>&1
 echo "ncu $tag rc=$?"

@@ -974,6 +974,7 @@ __global__ void __launch_bounds__(T) k_select(const __grid_constant__ StepArgs a
                                                             // (results use s_cand[0 .. BW))
   const int req = blockIdx.x, tid = threadIdx.x;
   if (req_sparse(a, req)) return;   // a mixed step's sparse-route request: k_sparse commits it
+  if (tid == 0 && a.seed_cnt) a.seed_cnt[req] = 0u;   // fused seed's arrival count / theta flag
   const uint64_t* src = a.surv + (size_t)req * a.cap;
   const uint64_t p0 = tid < a.cap ? src[tid] : 0ull;
   const uint64_t p1 = tid + T < a.cap ? src[tid + T] : 0ull;

@@ -160,7 +160,35 @@ struct Desc {
 // kModeSeedReq: the same seed with one CTA per request (its R0 seed rows in order): the histogram
 // lives in shared memory and the CTA derives theta itself at the end (no global histogram
 // atomics, no separate theta kernel).
-constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2, kModeSeedHist = 3, kModeSeedReq = 4;
+// kModeFused: the seed and the step in ONE launch. The row sequence is the R0 seed rows of every
+// request (request-major, seed work only), then every row (b-major, as kModeNormal). The last of a
+// request's seed rows to finish (per-request arrival counter) derives theta from the completed
+// histogram and publishes it (a.seed_cnt[req] = kSeedReady, release); a row that needs theta
+// before it is published waits for it (acquire), bounded: after ~10 ms it proceeds with no bound
+// (theta = -inf is always valid). Every CTA's seed rows precede its other rows, so a waiting CTA
+// never holds up a seed row.
+constexpr int kModeNormal = 0, kModeStats = 1, kModeShardEmit = 2, kModeSeedHist = 3, kModeSeedReq = 4,
+              kModeFused = 5;
+constexpr uint32_t kSeedReady = 0x80000000u;   // a.seed_cnt[req]: theta published (fused mode)
+
+// theta of request req once its seed has published it (fused mode; see kModeFused). Lane 0 of the
+// calling warp polls; the value is broadcast to the warp.
+__device__ __forceinline__ float fused_theta(const StepArgs& a, int req) {
+  uint32_t th = 0u;
+  if ((threadIdx.x & 31) == 0) {
+    for (int n = 0;; ++n) {
+      uint32_t f;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.seed_cnt + req) : "memory");
+      if (f == kSeedReady) {
+        th = __ldcg(a.theta + req);
+        break;
+      }
+      if (n > (1 << 16)) break;   // no bound for this row: always valid (more survivors)
+      __nanosleep(128);
+    }
+  }
+  return theta_value(__shfl_sync(0xffffffffu, th, 0));
+}
 
 // Consumer-group reductions: warp butterfly, then every consumer thread folds the per-warp
 // partials in a fixed order (bitwise-identical, deterministic results in every thread).
@@ -848,7 +876,10 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   static_assert(C == 1 || (G == 1 && (MODE == kModeNormal || MODE == kModeSeedHist)), "cluster: one group");
   constexpr bool SEED = MODE == kModeSeedHist || MODE == kModeSeedReq;
   constexpr bool SREQ = MODE == kModeSeedReq;
+  constexpr bool FUSED = MODE == kModeFused;   // seed_rows = R0 (seed rows per request)
+  constexpr bool EMIT = MODE == kModeNormal || FUSED;
   static_assert(!SREQ || (G == 1 && C == 1), "request-major seed: one group, no cluster");
+  static_assert(!FUSED || (G == 1 && C == 1), "fused seed: one group, no cluster");
   __shared__ uint32_t s_hist[SREQ ? kSeedBins : 1];   // request-major seed: this request's histogram
   constexpr int NXS = 4;           // cluster mailbox slots (the CTAs of a cluster are <= 1 row apart)
   __shared__ float2 mbox[NXS][C];
@@ -905,7 +936,11 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
   // w = b * n_dense + i of request dense_list[1 + i]
   const int ndl = (a.dense_list && !SREQ) ? a.dense_list[0] : a.batch;
   if (a.dense_list && !SREQ) total = ndl * (total / a.batch);
-  auto row_ok = [&](int k) { return SREQ ? k < total : cl + k * ncl < total; };
+  // fused: rows w < tseed are the seed rows (request i = w / r0f, b = w % r0f), then w - tseed b-major
+  const int r0f = FUSED ? min(seeded_rows, total / max(ndl, 1)) : 0;
+  const int tseed = ndl * r0f;
+  const int tall = total + tseed;
+  auto row_ok = [&](int k) { return SREQ ? k < total : cl + k * ncl < tall; };
 
   if (tid >= NC) {
     // ------------------------------- producer warp ---------------------------------------
@@ -916,7 +951,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     const uint64_t pol = policy_evict_first();
     const uint64_t pol_keep = policy_evict_last();
     struct Meta {
-      int b, req, live;
+      int b, req, live, seed;
       float S, th;
       uint32_t node;
       int slot;
@@ -924,24 +959,44 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     };
     auto fetch_raw = [&](int k0) {
       Meta m;
-      const int w = SREQ ? k0 + lane : cl + (k0 + lane) * ncl;
+      int w = SREQ ? k0 + lane : cl + (k0 + lane) * ncl;
+      bool srow = false;   // fused: a seed row
       m.b = 0;
       m.req = 0;
       m.live = 0;
+      m.seed = 0;
       m.S = 0.f;
       m.th = -INFINITY;
       m.node = 0;
       m.slot = -1;
       m.lse = 0.f;
-      if (w < total) {
-        m.b = SREQ ? w : w / ndl;
-        m.req = SREQ ? (int)blockIdx.x : w - m.b * ndl;
+      if (w < tall) {
+        if (FUSED && w < tseed) {
+          srow = true;
+          m.req = w / r0f;
+          m.b = w - m.req * r0f;
+        } else {
+          if (FUSED) w -= tseed;
+          m.b = SREQ ? w : w / ndl;
+          m.req = SREQ ? (int)blockIdx.x : w - m.b * ndl;
+        }
         if (a.dense_list && !SREQ) m.req = a.dense_list[1 + m.req];
         const int nl = a.nlive_in ? a.nlive_in[m.req] : 1;
         m.live = m.b < nl && !req_sparse(a, m.req);   // a mixed step's sparse-route requests: k_sparse
+        m.seed = srow;
         if (m.live) {
           row_state(a, m.req, m.b, m.S, m.node);
-          if (MODE != kModeStats && !SEED) m.th = theta_value(a.theta[m.req]);
+          if (FUSED) {
+            if (srow) {
+              m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
+            } else {   // theta if already published, else NaN: the consumer waits for it
+              uint32_t f;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.seed_cnt + m.req) : "memory");
+              m.th = f == kSeedReady ? theta_value(__ldcg(a.theta + m.req)) : __int_as_float(0x7fc00000);
+            }
+          } else if (MODE != kModeStats && !SEED) {
+            m.th = theta_value(a.theta[m.req]);
+          }
           if (SEED) m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
           if (MODE == kModeShardEmit) {
             bool fin;
@@ -967,15 +1022,19 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       fetch_slot(m1);
       // decisions for the current batch (its loads completed during the previous batch)
       int kind = 0;
-      if (m0.live && !(MODE == kModeShardEmit && m0.lse != m0.lse)) {
+      if (FUSED && m0.seed) {
+        // a live seed row always reaches the consumers (it must arrive); a sparse one adds its
+        // candidates by label there
+        if (m0.live) kind = 4 | (m0.slot >= 0 ? 1 : 2);
+      } else if (m0.live && !(MODE == kModeShardEmit && m0.lse != m0.lse)) {
         if (m0.S < m0.th) {   // every candidate of the row is <= S_b < theta: skip unread
           a.lse[(size_t)m0.req * BW + m0.b] = __int_as_float(0x7fc00000);
           if (a.counters_on && crank == 0) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
-        } else if (!(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
+        } else if (FUSED || !(m0.slot >= 0 && m0.b < seeded_rows)) {   // seeded dense rows are done
           kind = m0.slot >= 0 ? 1 : 2;
           // sparse-parent rows: gathered by label by one thread each in k_sparse_rows; in a cluster
           // only rank 0 handles them (the whole row) in the seed pass
-          if (kind == 2 && ((MODE == kModeNormal && a.defer_sparse) || crank != 0)) kind = 0;
+          if (kind == 2 && ((EMIT && a.defer_sparse) || crank != 0)) kind = 0;
         }
       }
       for (int j = 0; j < 32; ++j) {
@@ -1005,12 +1064,13 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           d.lse = jlse;
           desc[st] = d;
           s_th[st] = jth;
-          if (jkind == 1) {
+          if ((jkind & 3) == 1) {
             const TI* row = static_cast<const TI*>(a.logits) + (size_t)jreq * a.req_stride + (size_t)jb * a.ld +
                             (size_t)crank * Vc;
             const uint32_t rb = (uint32_t)Vc * (uint32_t)sizeof(TI), mb = (uint32_t)(Vc >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
-            bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], pol);
+            // a fused seed row is read again shortly (its step pass): keep it in L2
+            bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], (FUSED && (jkind & 4)) ? pol_keep : pol);
             // a dense node's bitmap is shared by every row whose beam sits on it: keep it in L2
             bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (ccol >> 5), mb, &full[st],
                      pol_keep);
@@ -1055,6 +1115,59 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
 #pragma unroll
     for (int i = 1; i < GT / 32; ++i) r += psum[i];
     return r;
+  };
+  // theta of request req from a histogram of d = S_0 - c (bins of 1/128), by this consumer group:
+  // the first bin where the count from the top reaches BW; theta = S_0 - (bin + 1)/128 - margin has
+  // >= BW candidates above it, so it is <= the request's BW-th best score (as k_seed_theta). A
+  // global histogram (fused mode: complete, every seed row arrived) is read from L2 and cleared.
+  auto group_theta = [&](uint32_t* h, bool global, int req) {
+    named_sync(bar_id, GT);
+    constexpr int PER = kSeedBins / GT;
+    uint32_t cc[PER], loc = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+      cc[j] = global ? __ldcg(h + lt * PER + j) : h[lt * PER + j];
+      loc += cc[j];
+    }
+    if (global) {
+#pragma unroll
+      for (int j = 0; j < PER; ++j) h[lt * PER + j] = 0u;   // ready for the next dense step
+    }
+    uint32_t incl = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    uint32_t* wtot = reinterpret_cast<uint32_t*>(s_tau[g]);
+    int* sbin = reinterpret_cast<int*>(&p_max[g][0]);
+    if (lane == 31) wtot[lt >> 5] = incl;
+    if (lt == 0) *sbin = -1;
+    named_sync(bar_id, GT);
+    uint32_t off = 0;
+    for (int w2 = 0; w2 < (lt >> 5); ++w2) off += wtot[w2];
+    incl += off;
+    uint32_t acc = incl - loc;
+    const uint32_t need = (uint32_t)(a.no_prune ? 0x7FFFFFFF : a.BW);
+    if (acc < need && incl >= need) {
+#pragma unroll
+      for (int j = 0; j < PER; ++j) {
+        if (acc < need && acc + cc[j] >= need) *sbin = lt * PER + j;
+        acc += cc[j];
+      }
+    }
+    named_sync(bar_id, GT);
+    if (lt == 0) {
+      uint32_t th = 0u;
+      if (*sbin >= 0) {
+        const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
+        th = f2o(S0 - (float)(*sbin + 1) * (1.0f / 128.0f) - 1e-5f * fmaxf(1.0f, fabsf(S0)));
+      }
+      a.theta[req] = th;
+      a.surv_count[req] = 0u;
+      a.ovf[req] = 0u;
+    }
+    named_sync(bar_id, GT);   // the scratch (s_tau, p_max) is free again
   };
   int it = 0;   // this group's dense-row count: parity selects the partials buffer
   // Deferred survivor emission: a warp reserves its slots with one atomicAdd whose result is
@@ -1112,13 +1225,16 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
     }
     const int req = d.req, b = d.b;
     const float S = d.S;
+    const bool srow = FUSED && (d.kind & 4);   // fused: a seed row (arrives below)
+    const int kind = d.kind & 3;
 
-    if (d.kind != 1) {
+    do {   // the row; `continue` ends it (then a fused seed row arrives)
+    if (kind != 1) {
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);
       // sparse seed rows add every candidate to the histogram (each is a real candidate, so the
       // count stays valid); with a per-beam Top-K cap they add nothing
-      if (d.kind == 0 || (SEED && a.topk)) continue;
+      if (kind == 0 || (SEED && a.topk)) continue;
       // sparse parent inside a dense step: gather the legal logits by label (rare)
       if (lt == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_READ, 1ull);
       const TI* row = static_cast<const TI*>(a.logits) + (size_t)req * a.req_stride + (size_t)b * a.ld - a.col0;
@@ -1155,7 +1271,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (lt == 0) a.stats_out[(size_t)req * BW + b] = M == -INFINITY ? make_float2(-INFINITY, 0.f) : make_float2(M, Z);
           continue;
         }
-        if (SEED) {
+        if (SEED || srow) {
           if (!((Z > 0.5f) && (Z <= 3.0e38f))) continue;   // the main pass flags the row
           const float lse2 = row_lse(M, Z), S0 = d.lse;
           uint32_t* h = SREQ ? s_hist : a.seed_hist + (size_t)req * kSeedBins;
@@ -1174,7 +1290,8 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         }
       }
       if (!finite) continue;
-      if (MODE == kModeNormal && !(cand_score(S, M, lse) >= th)) continue;
+      if (FUSED && th != th) th = fused_theta(a, req);
+      if (EMIT && !(cand_score(S, M, lse) >= th)) continue;
       const uint32_t fbase = (uint32_t)b * (uint32_t)V;
       for (uint32_t q0 = fc; q0 < fe; q0 += GT) {
         const uint32_t q = q0 + lt;
@@ -1315,7 +1432,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       }
       continue;
     }
-    if (SEED) {
+    if (SEED || srow) {
       // rows b < R0: candidates >= a row-local bound tau into the request's histogram of S_0 - c
       // (bins of 1/128). tau: each warp's m-th largest (m = ceil(BW / 8) <= 64) of its lanes'
       // top-2 candidates -- distinct elements, so the row has >= BW candidates >= tau.
@@ -1420,6 +1537,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       if (lane == 0) atomicAdd(a.counters + XGR_CNT_LEGAL, (unsigned long long)lc);
     }
     if (!finite) continue;
+    if (FUSED && th != th) th = fused_theta(a, req);   // not yet published when the row was fetched
     if (!(cand_score(S, M, lse) >= th)) {  // UB_b = S_b - ln Z_b < theta: nothing to emit
       if (lt == 0 && crank == 0 && a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_POST, 1ull);
       continue;
@@ -1510,56 +1628,36 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
       const int tot = __reduce_add_sync(0xffffffffu, ns);
       if (lane == 0 && tot) atomicAdd(a.counters + XGR_CNT_SURVIVORS, (unsigned long long)tot);
     }
+    } while (0);
+    if constexpr (FUSED) {
+      if (srow) {
+        // this seed row's histogram adds are done: arrive; the request's last seed row derives and
+        // publishes theta (fences: every thread's adds before the arrival, the arrival before the
+        // histogram reads, theta before the flag)
+        __threadfence();
+        named_sync(bar_id, GT);
+        int* slast = reinterpret_cast<int*>(&p_sum[g][0]);
+        if (lt == 0) {
+          const int nl = a.nlive_in ? a.nlive_in[req] : 1;
+          const uint32_t prev = atomicAdd(a.seed_cnt + req, 1u);
+          *slast = prev + 1 == (uint32_t)min(r0f, nl);
+        }
+        named_sync(bar_id, GT);
+        if (*slast) {
+          __threadfence();
+          group_theta(a.seed_hist + (size_t)req * kSeedBins, true, req);
+          if (lt == 0) {
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.seed_cnt + req), "r"(kSeedReady) : "memory");
+          }
+        } else {
+          named_sync(bar_id, GT);   // *slast read by every thread before its next reuse
+        }
+      }
+    }
   }
   flush();
-  if constexpr (SREQ) {
-    // theta of request blockIdx.x from its histogram of d = S_0 - c (bins of 1/128): the first bin
-    // where the count from the top reaches BW; theta = S_0 - (bin + 1)/128 - margin has >= BW
-    // candidates above it, so it is <= the request's BW-th best score (as k_seed_theta)
-    named_sync(bar_id, GT);
-    constexpr int PER = kSeedBins / GT;
-    uint32_t cc[PER], loc = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-      cc[j] = s_hist[lt * PER + j];
-      loc += cc[j];
-    }
-    uint32_t incl = loc;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    uint32_t* wtot = reinterpret_cast<uint32_t*>(s_tau[g]);
-    int* sbin = reinterpret_cast<int*>(&p_max[g][0]);
-    if (lane == 31) wtot[lt >> 5] = incl;
-    if (lt == 0) *sbin = -1;
-    named_sync(bar_id, GT);
-    uint32_t off = 0;
-    for (int w2 = 0; w2 < (lt >> 5); ++w2) off += wtot[w2];
-    incl += off;
-    uint32_t acc = incl - loc;
-    const uint32_t need = (uint32_t)(a.no_prune ? 0x7FFFFFFF : a.BW);
-    if (acc < need && incl >= need) {
-#pragma unroll
-      for (int j = 0; j < PER; ++j) {
-        if (acc < need && acc + cc[j] >= need) *sbin = lt * PER + j;
-        acc += cc[j];
-      }
-    }
-    named_sync(bar_id, GT);
-    if (lt == 0) {
-      const int req = blockIdx.x;
-      uint32_t th = 0u;
-      if (*sbin >= 0) {
-        const float S0 = a.score_in ? a.score_in[(size_t)req * a.BW] : 0.0f;
-        th = f2o(S0 - (float)(*sbin + 1) * (1.0f / 128.0f) - 1e-5f * fmaxf(1.0f, fabsf(S0)));
-      }
-      a.theta[req] = th;
-      a.surv_count[req] = 0u;
-      a.ovf[req] = 0u;
-    }
-  }
+  if constexpr (SREQ) group_theta(s_hist, false, (int)blockIdx.x);
   if (C > 1) cluster_sync_all();   // no CTA leaves while a peer may still write its mailbox
 }
 
@@ -1792,7 +1890,8 @@ static int g_seed_rows = 4;        // XGR_SEED_ROWS: 4 (default) or 2 seed rows 
 static int g_seed_kernel = 1;      // XGR_SEED_KERNEL: 1 k_seed_hist (one CTA per seed row, the row in
                                    // registers) + k_seed_theta (default: 1-2% faster passes at C3 / C2),
                                    // 2 b-major streamed seed (k_stream seed mode) + k_seed_theta,
-                                   // 0 request-major seed with theta in the same kernel
+                                   // 0 request-major seed with theta in the same kernel,
+                                   // 3 k_seed_hist_theta, 4 seed + step in one launch (kModeFused)
 static int g_seed_mode = 1;        // XGR_SEED_MODE: 1 histogram seed (default), 0 exact union seed (k_seed)
 
 template <typename K>
@@ -1942,6 +2041,7 @@ cudaError_t configure_stream_kernels() {
   if (const char* v = getenv("XGR_SEED_MODE")) g_seed_mode = atoi(v);
   if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
+  if ((e = opt_in(k_stream<32, 1, 2, 3, kModeFused>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 3, 2, kModeSeedReq>, stream_smem<32, 3>())) != cudaSuccess) return e;
 
   if ((e = opt_in(k_stream<32, 1, 4, 2, kModeSeedReq, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
@@ -2040,6 +2140,17 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
                  stream_smem<32, 4, bf, 512>(), s, a, total, 0);
     if (ev1) cudaEventRecord(ev1, s);
     *launches += 2;
+    return cudaGetLastError();
+  }
+  if (a.trie.V <= 8192 && g_seed_kernel == 4 && g_seed_mode >= 1 && !a.topk && !a.gstats &&
+      std::min(a.theta_rows, rows) > 0) {
+    // the seed and the step in one persistent launch (kModeFused)
+    const int r0 = std::min(a.theta_rows, rows);
+    if (ev0) cudaEventRecord(ev0, s);
+    launch_pdl(k_stream<32, 1, 2, 3, kModeFused>, std::min(total + a.batch * r0, 3 * sms), 256 + 32,
+               stream_smem<32, 2>(), s, a, total, r0);
+    if (ev1) cudaEventRecord(ev1, s);
+    *launches += 1;
     return cudaGetLastError();
   }
   if (a.trie.V <= 8192) {

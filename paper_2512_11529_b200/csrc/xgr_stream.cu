@@ -1037,10 +1037,13 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (kind == 2 && ((EMIT && a.defer_sparse) || crank != 0)) kind = 0;
         }
       }
+      // fused: theta of the batch's next row, re-read (acquire) by lane 0 right after issuing the
+      // current row when it was not yet published at fetch time (loads complete during the wait)
+      float pth = __int_as_float(0x7fc00000);
       for (int j = 0; j < 32; ++j) {
         const int kj = k0 + j;
         if (!row_ok(kj)) break;
-        const int jkind = __shfl_sync(0xffffffffu, kind, j);
+        int jkind = __shfl_sync(0xffffffffu, kind, j);
         const int jslot = __shfl_sync(0xffffffffu, m0.slot, j);
         const int jb = __shfl_sync(0xffffffffu, m0.b, j);
         const int jreq = __shfl_sync(0xffffffffu, m0.req, j);
@@ -1048,11 +1051,27 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         const float jth = __shfl_sync(0xffffffffu, m0.th, j);
         const uint32_t jnode = __shfl_sync(0xffffffffu, m0.node, j);
         const float jlse = __shfl_sync(0xffffffffu, m0.lse, j);
+        int nkind = 0, nreq = 0;
+        float nth = 0.f;
+        if (FUSED) {
+          nkind = __shfl_sync(0xffffffffu, kind, (j + 1) & 31);
+          nreq = __shfl_sync(0xffffffffu, m0.req, (j + 1) & 31);
+          nth = __shfl_sync(0xffffffffu, m0.th, (j + 1) & 31);
+        }
         if (lane == 0) {
           const int st = R::stage(kj), u = R::use(kj);
           if (u > 0) {   // the stage's previous row (same group) has been consumed
             if (a.dbg & 4096) mbar_wait(&empty[st], (u - 1) & 1);
             else mbar_wait_sleep(&empty[st], (u - 1) & 1);
+          }
+          float jth_use = jth;
+          if (FUSED && jth != jth && jkind != 0 && !(jkind & 4)) {
+            jth_use = pth;   // NaN if still unpublished: the consumers wait for it
+            if (jS < jth_use) {   // now known to be below theta: skip unread
+              a.lse[(size_t)jreq * BW + jb] = __int_as_float(0x7fc00000);
+              if (a.counters_on) atomicAdd(a.counters + XGR_CNT_ROWS_SKIP_PRE, 1ull);
+              jkind = 0;
+            }
           }
           Desc d;
           d.req = jreq;
@@ -1063,7 +1082,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           d.node = jnode;
           d.lse = jlse;
           desc[st] = d;
-          s_th[st] = jth;
+          s_th[st] = jth_use;
           if ((jkind & 3) == 1) {
             const TI* row = static_cast<const TI*>(a.logits) + (size_t)jreq * a.req_stride + (size_t)jb * a.ld +
                             (size_t)crank * Vc;
@@ -1076,6 +1095,14 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
                      pol_keep);
           } else {
             mbar_arrive(&full[st]);
+          }
+          if (FUSED) {
+            pth = __int_as_float(0x7fc00000);
+            if (j < 31 && nkind != 0 && !(nkind & 4) && nth != nth) {
+              uint32_t f;
+              asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.seed_cnt + nreq) : "memory");
+              if (f == kSeedReady) pth = theta_value(__ldcg(a.theta + nreq));
+            }
           }
         }
         __syncwarp();

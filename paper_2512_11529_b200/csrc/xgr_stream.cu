@@ -989,10 +989,12 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           if (FUSED) {
             if (srow) {
               m.lse = a.score_in ? a.score_in[(size_t)m.req * BW] : 0.0f;   // S_0
-            } else {   // theta if already published, else NaN: the consumer waits for it
+            } else if (!(a.dbg & (1 << 25))) {   // theta if already published, else NaN: the consumer waits
               uint32_t f;
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.seed_cnt + m.req) : "memory");
               m.th = f == kSeedReady ? theta_value(__ldcg(a.theta + m.req)) : __int_as_float(0x7fc00000);
+            } else {
+              m.th = __int_as_float(0x7fc00000);
             }
           } else if (MODE != kModeStats && !SEED) {
             m.th = theta_value(a.theta[m.req]);
@@ -1089,7 +1091,8 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
             const uint32_t rb = (uint32_t)Vc * (uint32_t)sizeof(TI), mb = (uint32_t)(Vc >> 5) * 4u;
             mbar_arrive_tx(&full[st], rb + mb);
             // a fused seed row is read again shortly (its step pass): keep it in L2
-            bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st], (FUSED && (jkind & 4)) ? pol_keep : pol);
+            bulk_g2s(s_row + (size_t)st * VT, row, rb, &full[st],
+                     (FUSED && (jkind & 4) && !(a.dbg & (1 << 27))) ? pol_keep : pol);
             // a dense node's bitmap is shared by every row whose beam sits on it: keep it in L2
             bulk_g2s(s_msk + (size_t)st * MW, L.bitmap + (size_t)jslot * W + (ccol >> 5), mb, &full[st],
                      pol_keep);
@@ -1098,7 +1101,7 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
           }
           if (FUSED) {
             pth = __int_as_float(0x7fc00000);
-            if (j < 31 && nkind != 0 && !(nkind & 4) && nth != nth) {
+            if (j < 31 && nkind != 0 && !(nkind & 4) && nth != nth && !(a.dbg & (1 << 26))) {
               uint32_t f;
               asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(a.seed_cnt + nreq) : "memory");
               if (f == kSeedReady) pth = theta_value(__ldcg(a.theta + nreq));
@@ -1661,10 +1664,11 @@ __global__ void __launch_bounds__(GT * G + 32, MINB) k_stream(const __grid_const
         // this seed row's histogram adds are done: arrive; the request's last seed row derives and
         // publishes theta (fences: every thread's adds before the arrival, the arrival before the
         // histogram reads, theta before the flag)
-        __threadfence();
+        if (!(a.dbg & (1 << 28))) __threadfence();
         named_sync(bar_id, GT);
         int* slast = reinterpret_cast<int*>(&p_sum[g][0]);
         if (lt == 0) {
+          if (a.dbg & (1 << 28)) __threadfence();   // cumulative: the group's adds, ordered by the barrier
           const int nl = a.nlive_in ? a.nlive_in[req] : 1;
           const uint32_t prev = atomicAdd(a.seed_cnt + req, 1u);
           *slast = prev + 1 == (uint32_t)min(r0f, nl);

@@ -615,7 +615,7 @@ def e2e(args, cfg, plan, run, logits, world, dev, cand):
     del hl
     return {"value": cand * ke / e2e_s, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s * 1e3 / ke, "steps": ke,
-            "path": "BeamSearch.step(pinned host tensor) -> H2D on the step stream -> xgr_beam_step; "
+            "path": "BeamSearch.step(pinned host tensor) -> xgr_beam_step_host (H2D on the step stream inside the C ABI); "
                     "xgr_beam_finalize(host outputs)"}
 
 

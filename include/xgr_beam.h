@@ -44,7 +44,7 @@
 extern "C" {
 #endif
 
-#define XGR_ABI_VERSION 1
+#define XGR_ABI_VERSION 2   /* 2: xgr_config allocator hooks, xgr_beam_step_host */
 
 typedef struct xgr_ctx xgr_ctx; /* opaque; one per in-flight batch */
 
@@ -88,6 +88,15 @@ typedef struct {
   int32_t survivor_cap; /* per-request survivor buffer (keys); 0 = min(32*BW, 16384)      */
   int32_t theta_rows;   /* rows 0..theta_rows-1 seed the threshold; 0 = default (8)       */
   uint32_t flags;       /* XGR_CFG_*                                                      */
+  /* Device-memory hooks, e.g. a framework's caching allocator; both or neither
+   * (NULL, NULL: cudaMalloc / cudaFree). dev_alloc(bytes, alloc_user) returns >= 16-byte aligned
+   * device memory on cfg.device or NULL (-> XGR_ERR_OOM); dev_free(ptr, alloc_user) takes it back.
+   * Called only from xgr_beam_init, xgr_mask_build, the support calls that need scratch
+   * (xgr_mask_children, xgr_beam_account), a growing xgr_beam_step_host and xgr_beam_destroy
+   * (which synchronises the device first) -- never from a step, so steps stay graph-capturable. */
+  void* (*dev_alloc)(size_t bytes, void* alloc_user);
+  void (*dev_free)(void* ptr, void* alloc_user);
+  void* alloc_user;
   int32_t reserved[5];  /* must be zero                                                   */
 } xgr_config;
 
@@ -134,6 +143,17 @@ xgr_status xgr_beam_step(xgr_ctx* ctx, int32_t batch, const float* logits, int32
  * other dtype or a sharded ctx. XGR_DTYPE_F32 is exactly xgr_beam_step. */
 xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int32_t dtype,
                             int32_t rows, int64_t ld, void* stream);
+
+/* xgr_beam_step_ex with the logits in HOST memory (the end-to-end path: PAPER.md L376, logits
+ * arrive from the model every step): the call copies host_logits [batch][rows][ld] (dtype
+ * elements, ld >= V) into a ctx-owned device staging buffer with cudaMemcpyAsync on `stream`,
+ * then enqueues the step on it. Use page-locked host memory for an asynchronous copy (pageable
+ * memory makes the copy synchronous). The staging buffer holds one step: the next
+ * xgr_beam_step_host on the same stream is ordered after this step's kernels. The first call, and
+ * any call needing a larger buffer, synchronises `stream` and allocates (not graph-capturable
+ * then); later calls only enqueue. Errors: as xgr_beam_step_ex; XGR_ERR_OOM. */
+xgr_status xgr_beam_step_host(xgr_ctx* ctx, int32_t batch, const void* host_logits, int32_t dtype,
+                              int32_t rows, int64_t ld, void* stream);
 
 /* After exactly nd steps: item tuples of the final beams, in slot order (score descending).
  * The last step's kernels already wrote them into ctx-owned device buffers (fused finalize);

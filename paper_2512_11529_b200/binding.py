@@ -35,7 +35,14 @@ EXPORTS = ["xgr_beam_init", "xgr_mask_build", "xgr_beam_step", "xgr_beam_step_ex
            "xgr_beam_counters", "xgr_beam_account", "xgr_beam_launch_count",
            "xgr_beam_kernel_times", "xgr_beam_outputs", "xgr_shard_stats", "xgr_shard_select",
            "xgr_shard_merge", "xgr_kv_reorder", "xgr_beam_step_head", "xgr_beam_next_route",
-           "xgr_attn_staged", "xgr_attn_shared", "xgr_attn_unshared", "xgr_attn_merge"]
+           "xgr_attn_staged", "xgr_attn_shared", "xgr_attn_unshared", "xgr_attn_merge",
+           "xgr_beam_step_host"]
+
+ABI_VERSION = 2
+
+# xgr_config.dev_alloc / dev_free
+DEV_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p)
+DEV_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p)
 
 
 class XgrConfig(ctypes.Structure):
@@ -44,7 +51,8 @@ class XgrConfig(ctypes.Structure):
         ("top_k", ctypes.c_int32), ("max_batch", ctypes.c_int32), ("device", ctypes.c_int32),
         ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
         ("survivor_cap", ctypes.c_int32), ("theta_rows", ctypes.c_int32),
-        ("flags", ctypes.c_uint32), ("reserved", ctypes.c_int32 * 5),
+        ("flags", ctypes.c_uint32), ("dev_alloc", DEV_ALLOC_FN), ("dev_free", DEV_FREE_FN),
+        ("alloc_user", ctypes.c_void_p), ("reserved", ctypes.c_int32 * 5),
     ]
 
 
@@ -66,6 +74,7 @@ def _load():
         "xgr_mask_build": [VP, VP, I64, VP],
         "xgr_beam_step": [VP, I32, VP, I32, I64, VP],
         "xgr_beam_step_ex": [VP, I32, VP, I32, I32, I64, VP],
+        "xgr_beam_step_host": [VP, I32, VP, I32, I32, I64, VP],
         "xgr_beam_finalize": [VP, VP, VP, VP, VP, I32, VP],
         "xgr_beam_destroy": [VP],
         "xgr_beam_view": [VP, P(VP), P(VP), P(VP), P(VP), P(VP)],
@@ -100,6 +109,9 @@ def _load():
     lib.xgr_beam_launch_count.restype = ctypes.c_int64
     lib.xgr_abi_version.argtypes = []
     lib.xgr_abi_version.restype = ctypes.c_int32
+    if lib.xgr_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI version {lib.xgr_abi_version()}, binding expects {ABI_VERSION} "
+                          "(rebuild: python -c 'import __graft_entry__ as g; g.build()')")
     return lib
 
 
@@ -137,6 +149,10 @@ XGR_DTYPE_F32, XGR_DTYPE_BF16 = 0, 1
 
 def xgr_beam_step_ex(ctx, batch, logits_ptr, dtype, rows, ld, stream=0):
     _check(lib.xgr_beam_step_ex(ctx, batch, logits_ptr, dtype, rows, ld, stream))
+
+
+def xgr_beam_step_host(ctx, batch, host_ptr, dtype, rows, ld, stream=0):
+    _check(lib.xgr_beam_step_host(ctx, batch, host_ptr, dtype, rows, ld, stream))
 
 
 def xgr_beam_finalize(ctx, tokens, item_rank, score, n_live, outputs_on_device, stream=0):
@@ -190,11 +206,31 @@ class BeamSearch:
 
     def __init__(self, vocab: int, nd: int, beam_width: int, max_batch: int, device: int = 0,
                  flags: int = 0, survivor_cap: int = 0, theta_rows: int = 0, top_k: int = 0,
-                 nranks: int = 1, rank: int = 0):
+                 nranks: int = 1, rank: int = 0, allocator=None):
+        """allocator: None (cudaMalloc) or "torch": the ctx's device memory comes from torch's
+        caching allocator (xgr_config.dev_alloc / dev_free)."""
         import torch
         self.vocab, self.nd, self.bw, self.max_batch = vocab, nd, beam_width, max_batch
         self.device = torch.device("cuda", device)
         cfg = XgrConfig()
+        self.alloc_calls = [0, 0]   # (allocations, frees) through the hooks
+        if allocator == "torch":
+            def _alloc(nbytes, _user):
+                self.alloc_calls[0] += 1
+                try:
+                    return torch.cuda.caching_allocator_alloc(int(nbytes), device)
+                except RuntimeError:
+                    return None   # -> XGR_ERR_OOM
+
+            def _free(ptr, _user):
+                self.alloc_calls[1] += 1
+                torch.cuda.caching_allocator_delete(ptr)
+
+            # the callbacks must outlive the ctx
+            self._hooks = (DEV_ALLOC_FN(_alloc), DEV_FREE_FN(_free))
+            cfg.dev_alloc, cfg.dev_free = self._hooks
+        elif allocator is not None:
+            raise ValueError("allocator must be None or 'torch'")
         cfg.vocab, cfg.nd, cfg.beam_width, cfg.top_k = vocab, nd, beam_width, top_k
         cfg.max_batch, cfg.device, cfg.nranks, cfg.rank = max_batch, device, nranks, rank
         self.nranks, self.rank = nranks, rank
@@ -202,7 +238,6 @@ class BeamSearch:
         self.ctx = xgr_beam_init(cfg)
         self.batch = None
         self.t = 0
-        self._staging = None
 
     def close(self):
         if self.ctx:
@@ -231,26 +266,18 @@ class BeamSearch:
         return xgr_mask_children(self.ctx, np.asarray(prefixes), depth, cap, self._stream())
 
     def step(self, logits, stream=None):
-        """logits: fp32 or bf16 [batch][rows][ld] (or [batch][rows][V]); CUDA tensor, or a pinned
-        CPU tensor, which is copied into a device staging buffer on the same stream first."""
+        """logits: fp32 or bf16 [batch][rows][ld] (or [batch][rows][V]); CUDA tensor
+        (xgr_beam_step_ex), or a CPU tensor -- pinned for an asynchronous copy -- which the library
+        copies into its device staging buffer on the same stream (xgr_beam_step_host)."""
         import torch
         if logits.dim() != 3 or logits.dtype not in (torch.float32, torch.bfloat16):
             raise ValueError("logits must be fp32 or bf16 [batch][rows][ld]")
         if logits.stride(2) != 1 or logits.stride(0) != logits.stride(1) * logits.shape[1]:
             raise ValueError("logits must be row-major [batch][rows][ld] (unit column stride)")
-        if not logits.is_cuda:
-            n = logits.numel() * logits.element_size()
-            if self._staging is None or self._staging.numel() < n:
-                self._staging = torch.empty(n, dtype=torch.uint8, device=self.device)
-            dev = self._staging[:n].view(logits.dtype).view(logits.shape)
-            s = stream if stream is not None else torch.cuda.current_stream()
-            with torch.cuda.stream(s):
-                dev.copy_(logits, non_blocking=True)
-            logits = dev
         b, rows = logits.shape[0], logits.shape[1]
         dt = XGR_DTYPE_BF16 if logits.dtype == torch.bfloat16 else XGR_DTYPE_F32
-        xgr_beam_step_ex(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), dt, rows, logits.stride(1),
-                         self._stream(stream))
+        step = xgr_beam_step_ex if logits.is_cuda else xgr_beam_step_host
+        step(self.ctx, b, ctypes.c_void_p(logits.data_ptr()), dt, rows, logits.stride(1), self._stream(stream))
         self.batch = b
         self.t += 1
 

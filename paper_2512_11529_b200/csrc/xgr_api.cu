@@ -44,6 +44,9 @@ using namespace xgr;
 
 struct xgr_ctx {
   xgr_config cfg;
+  DevAlloc al;                      // cfg.dev_alloc / dev_free, else cudaMalloc / cudaFree
+  void* host_stage = nullptr;       // xgr_beam_step_host: device copy of the step's logits
+  size_t host_stage_bytes = 0;
   int V = 0, nd = 0, BW = 0, maxB = 0, cap = 0, R0 = 0, K = 0;
   TrieHost trie;
   bool built = false;
@@ -122,38 +125,43 @@ static xgr_status fail(xgr_status st, const char* fmt, ...) {
   } while (0)
 
 static void ctx_free(xgr_ctx* c) {
+  // a caller's allocator may hand the memory to other work at once: nothing of this ctx may still run
+  if (c->al.release) cudaDeviceSynchronize();
   for (auto e : c->ev) cudaEventDestroy(e);
   c->ev.clear();
   trie_free(c->trie);
+  c->al.put(c->host_stage);
+  c->host_stage = nullptr;
+  c->host_stage_bytes = 0;
   for (int i = 0; i < 2; ++i) {
-    cudaFree(c->score[i]);
-    cudaFree(c->node[i]);
-    cudaFree(c->nlive[i]);
+    c->al.put(c->score[i]);
+    c->al.put(c->node[i]);
+    c->al.put(c->nlive[i]);
   }
-  cudaFree(c->parent_hist);
-  cudaFree(c->token_hist);
-  cudaFree(c->d_phist);
-  cudaFree(c->d_thist);
-  cudaFree(c->scratch);
-  cudaFree(c->ph_lists);
-  cudaFree(c->ph_cnt);
-  cudaFree(c->dense_list);
-  cudaFree(c->next_keys[0]);
-  cudaFree(c->next_keys[1]);
-  cudaFree(c->seed_hist);
-  cudaFree(c->seed_cnt);
-  cudaFree(c->head_logits);
-  cudaFree(c->surv);
-  cudaFree(c->lse);
-  cudaFree(c->flags);
-  cudaFree(c->counters);
-  cudaFree(c->out_tokens);
-  cudaFree(c->out_rank);
-  cudaFree(c->out_score);
-  cudaFree(c->out_nlive);
-  cudaFree(c->shard_stats);
-  cudaFree(c->shard_rec);
-  cudaFree(c->shard_rec_n);
+  c->al.put(c->parent_hist);
+  c->al.put(c->token_hist);
+  c->al.put(c->d_phist);
+  c->al.put(c->d_thist);
+  c->al.put(c->scratch);
+  c->al.put(c->ph_lists);
+  c->al.put(c->ph_cnt);
+  c->al.put(c->dense_list);
+  c->al.put(c->next_keys[0]);
+  c->al.put(c->next_keys[1]);
+  c->al.put(c->seed_hist);
+  c->al.put(c->seed_cnt);
+  c->al.put(c->head_logits);
+  c->al.put(c->surv);
+  c->al.put(c->lse);
+  c->al.put(c->flags);
+  c->al.put(c->counters);
+  c->al.put(c->out_tokens);
+  c->al.put(c->out_rank);
+  c->al.put(c->out_score);
+  c->al.put(c->out_nlive);
+  c->al.put(c->shard_stats);
+  c->al.put(c->shard_rec);
+  c->al.put(c->shard_rec_n);
 }
 
 namespace xgr {
@@ -198,6 +206,8 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   if (c.survivor_cap < 0 || c.theta_rows < 0) return fail(XGR_ERR_INVALID_ARG, "init: negative knob");
   for (int i = 0; i < 5; ++i)
     if (c.reserved[i]) return fail(XGR_ERR_INVALID_ARG, "init: reserved fields must be zero");
+  if (!c.dev_alloc != !c.dev_free)
+    return fail(XGR_ERR_INVALID_ARG, "init: dev_alloc and dev_free must be given together");
   if ((c.flags & XGR_CFG_PAPER_HEAP) && (c.vocab > 16384 || c.nranks > 1))
     return fail(XGR_ERR_UNSUPPORTED, "init: the paper-heap baseline needs vocab <= 16384 and no codebook shard");
   if (c.flags & ~(XGR_CFG_NO_PRUNE | XGR_CFG_COUNTERS | XGR_CFG_NO_SPARSE_KERNEL | XGR_CFG_TIMING | XGR_CFG_PAPER_HEAP))
@@ -229,7 +239,11 @@ xgr_status xgr_beam_init(const xgr_config* cfg, xgr_ctx** out) {
   x->R0 = c.theta_rows ? c.theta_rows : 8;
   x->K = (c.top_k > 0 && c.top_k < c.beam_width) ? c.top_k : 0;   // 0: no per-beam truncation
   const size_t nb = (size_t)x->maxB * x->BW;
-  auto al = [&](void** p, size_t bytes) -> cudaError_t { return cudaMalloc(p, std::max<size_t>(bytes, 16)); };
+  x->al.alloc = c.dev_alloc;
+  x->al.release = c.dev_free;
+  x->al.user = c.alloc_user;
+  x->trie.al = x->al;
+  auto al = [&](void** p, size_t bytes) -> cudaError_t { return x->al.get(p, bytes); };
   cudaError_t e = cudaSuccess;
   for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
     e = al((void**)&x->score[i], nb * 4);
@@ -463,6 +477,30 @@ xgr_status xgr_beam_step_ex(xgr_ctx* ctx, int32_t batch, const void* logits, int
   return XGR_OK;
 }
 
+xgr_status xgr_beam_step_host(xgr_ctx* ctx, int32_t batch, const void* host_logits, int32_t dtype, int32_t rows,
+                              int64_t ld, void* stream) {
+  NvtxRange nvtx_("xgr_beam_step_host");
+  if (!ctx) return fail(XGR_ERR_INVALID_ARG, "step_host: ctx is NULL");
+  if (!host_logits) return fail(XGR_ERR_INVALID_ARG, "step_host: logits is NULL");
+  if (dtype != XGR_DTYPE_F32 && dtype != XGR_DTYPE_BF16)
+    return fail(XGR_ERR_UNSUPPORTED, "step_host: dtype %d", dtype);
+  if (batch < 1 || batch > ctx->maxB || rows < 1 || ld < ctx->V)
+    return fail(XGR_ERR_INVALID_ARG, "step_host: batch %d, rows %d, ld %lld out of range", batch, rows, (long long)ld);
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t bytes = (size_t)batch * rows * ld * (dtype == XGR_DTYPE_BF16 ? 2 : 4);
+  if (bytes > ctx->host_stage_bytes) {
+    // grow the staging buffer: kernels enqueued earlier may still read the old one
+    ACK(cudaStreamSynchronize(s));
+    ctx->al.put(ctx->host_stage);
+    ctx->host_stage = nullptr;
+    ctx->host_stage_bytes = 0;
+    ACK(ctx->al.get(&ctx->host_stage, bytes));
+    ctx->host_stage_bytes = bytes;
+  }
+  ACK(cudaMemcpyAsync(ctx->host_stage, host_logits, bytes, cudaMemcpyHostToDevice, s));
+  return xgr_beam_step_ex(ctx, batch, ctx->host_stage, dtype, rows, ld, stream);
+}
+
 // ---- LM-head fusion at sparse steps (NEXT f4) ------------------------------------------------------
 
 static bool next_is_sparse(const xgr_ctx* ctx, int64_t* keys) {
@@ -674,18 +712,18 @@ xgr_status xgr_mask_children(const xgr_ctx* ctx, const int32_t* prefixes, int32_
   if (n == 0) return XGR_OK;
   cudaStream_t s = (cudaStream_t)stream;
   int32_t *dp = nullptr, *dc = nullptr, *dt = nullptr;
-  ACK(cudaMalloc(&dp, std::max<size_t>(16, (size_t)n * depth * 4)));
-  ACK(cudaMalloc(&dc, (size_t)n * 4));
-  ACK(cudaMalloc(&dt, std::max<size_t>(16, (size_t)n * cap * 4)));
+  ACK(ctx->al.get(&dp, (size_t)n * depth * 4));
+  ACK(ctx->al.get(&dc, (size_t)n * 4));
+  ACK(ctx->al.get(&dt, (size_t)n * cap * 4));
   cudaError_t e = cudaSuccess;
   if (depth > 0) e = cudaMemcpyAsync(dp, prefixes, (size_t)n * depth * 4, cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess) e = launch_children(trie_dev(ctx->trie), dp, depth, n, dc, dt, cap, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(counts, dc, (size_t)n * 4, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess && cap > 0) e = cudaMemcpyAsync(tokens, dt, (size_t)n * cap * 4, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(dp);
-  cudaFree(dc);
-  cudaFree(dt);
+  ctx->al.put(dp);
+  ctx->al.put(dc);
+  ctx->al.put(dt);
   if (e != cudaSuccess) return fail(XGR_ERR_CUDA, "mask_children: %s", cudaGetErrorString(e));
   return XGR_OK;
 }
@@ -721,16 +759,16 @@ xgr_status xgr_beam_account(xgr_ctx* ctx, int64_t* alg_bytes, int64_t* full_byte
   const int64_t nd_dense = std::max<int64_t>(ctx->trie.lv[ctx->last.level].n_dense, 1);
   uint32_t* touched = nullptr;
   unsigned long long* dout = nullptr;
-  ACK(cudaMalloc(&touched, ((nd_dense + 31) / 32) * 4));
-  ACK(cudaMalloc(&dout, 3 * 8));
+  ACK(ctx->al.get(&touched, ((nd_dense + 31) / 32) * 4));
+  ACK(ctx->al.get(&dout, 3 * 8));
   unsigned long long h[3] = {0, 0, 0};
   cudaError_t e = cudaMemsetAsync(touched, 0, ((nd_dense + 31) / 32) * 4, s);
   if (e == cudaSuccess) e = cudaMemsetAsync(dout, 0, 3 * 8, s);
   if (e == cudaSuccess) e = launch_account(ctx->last, ctx->last_rows, touched, dout, s);
   if (e == cudaSuccess) e = cudaMemcpyAsync(h, dout, 3 * 8, cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(touched);
-  cudaFree(dout);
+  ctx->al.put(touched);
+  ctx->al.put(dout);
   if (e != cudaSuccess) return fail(XGR_ERR_CUDA, "account: %s", cudaGetErrorString(e));
   if (alg_bytes) *alg_bytes = (int64_t)h[0];
   if (full_bytes) *full_bytes = (int64_t)h[1];

@@ -23,11 +23,11 @@ namespace xgr {
 
 void trie_free(TrieHost& t) {
   for (auto& L : t.lv) {
-    cudaFree(L.first_child);
-    cudaFree(L.label);
-    cudaFree(L.dense_slot);
-    cudaFree(L.bitmap);
-    cudaFree(L.rankdir);
+    t.al.put(L.first_child);
+    t.al.put(L.label);
+    t.al.put(L.dense_slot);
+    t.al.put(L.bitmap);
+    t.al.put(L.rankdir);
     L = LevelHost();
   }
   t.bytes = 0;
@@ -175,11 +175,11 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
   int64_t prev_nodes = 1;
 
   const int64_t chunk = 1 << 24;
-  BCK(cudaMalloc(&k0, n * sizeof(uint64_t)));
-  BCK(cudaMalloc(&k1, n * sizeof(uint64_t)));
-  BCK(cudaMalloc(&d_items, std::min(n, chunk) * nd * sizeof(int32_t)));
-  BCK(cudaMalloc(&d_err, 2 * sizeof(uint32_t)));
-  BCK(cudaMalloc(&d_maxc, sizeof(int32_t)));
+  BCK(out.al.get(&k0, n * sizeof(uint64_t)));
+  BCK(out.al.get(&k1, n * sizeof(uint64_t)));
+  BCK(out.al.get(&d_items, std::min(n, chunk) * nd * sizeof(int32_t)));
+  BCK(out.al.get(&d_err, 2 * sizeof(uint32_t)));
+  BCK(out.al.get(&d_maxc, sizeof(int32_t)));
   d_num = d_err + 1;
   BCK(cudaMemsetAsync(d_err, 0, 2 * sizeof(uint32_t), s));
   for (int64_t c0 = 0; c0 < n; c0 += chunk) {
@@ -191,7 +191,7 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
   }
   BCK(cudaMemcpyAsync(&h_err, d_err, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
   BCK(cudaStreamSynchronize(s));
-  cudaFree(d_items);
+  out.al.put(d_items);
   d_items = nullptr;
   if (h_err) {
     err = "mask_build: a token is < 0 or >= V";
@@ -207,7 +207,7 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
     BCK(cub::DeviceSelect::Unique(nullptr, b2, k1, k0, d_num, (int64_t)n, s));
     BCK(cub::DeviceScan::InclusiveSum(nullptr, b3, (uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)n, s));
     temp_bytes = std::max(b1, std::max(b2, b3));
-    BCK(cudaMalloc(&temp, temp_bytes));
+    BCK(out.al.get(&temp, temp_bytes));
     BCK(cub::DeviceRadixSort::SortKeys(temp, b1, db, (int64_t)n, 0, w * nd, s));
     uint64_t* sorted = db.Current();
     uint64_t* other = db.Alternate();
@@ -219,14 +219,14 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
     BCK(cudaStreamSynchronize(s));
     N = hn;
   }
-  cudaFree(k1);
+  out.al.put(k1);
   k1 = nullptr;
   out.n_items = N;
   out.lv[0].n_nodes = 1;
 
-  BCK(cudaMalloc(&starts, N * sizeof(uint32_t)));
-  BCK(cudaMalloc(&id_d, N * sizeof(uint32_t)));
-  BCK(cudaMalloc(&id_p, N * sizeof(uint32_t)));
+  BCK(out.al.get(&starts, N * sizeof(uint32_t)));
+  BCK(out.al.get(&id_d, N * sizeof(uint32_t)));
+  BCK(out.al.get(&id_p, N * sizeof(uint32_t)));
   for (int d = 1; d <= nd; ++d) {
     int shift_d = w * (nd - d);
     int shift_p = (d == 1) ? 64 : w * (nd - d + 1);
@@ -241,11 +241,11 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
     LevelHost& P = out.lv[d - 1];
     LevelHost& C = out.lv[d];
     C.n_nodes = nodes;
-    BCK(cudaMalloc(&C.label, nodes * sizeof(uint16_t)));
-    BCK(cudaMalloc(&P.first_child, (prev_nodes + 1) * sizeof(uint32_t)));
-    cudaFree(parent);
+    BCK(out.al.get(&C.label, nodes * sizeof(uint16_t)));
+    BCK(out.al.get(&P.first_child, (prev_nodes + 1) * sizeof(uint32_t)));
+    out.al.put(parent);
     parent = nullptr;
-    BCK(cudaMalloc(&parent, nodes * sizeof(uint32_t)));
+    BCK(out.al.get(&parent, nodes * sizeof(uint32_t)));
     {
       uint32_t nn = (uint32_t)nodes;
       BCK(cudaMemcpyAsync(P.first_child + prev_nodes, &nn, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
@@ -256,9 +256,9 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
     // parent level: child counts, dense set, slots
     {
       uint32_t thr = (uint32_t)std::max(1, V / 16);
-      cudaFree(tmp);
+      out.al.put(tmp);
       tmp = nullptr;
-      BCK(cudaMalloc(&tmp, 2 * (prev_nodes + 1) * sizeof(uint32_t)));
+      BCK(out.al.get(&tmp, 2 * (prev_nodes + 1) * sizeof(uint32_t)));
       uint32_t* flag = tmp;
       uint32_t* excl = tmp + prev_nodes + 1;
       BCK(cudaMemsetAsync(d_maxc, 0, sizeof(int32_t), s));
@@ -267,10 +267,10 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
       size_t b4 = 0;
       BCK(cub::DeviceScan::ExclusiveSum(nullptr, b4, flag, excl, (int64_t)prev_nodes + 1, s));
       if (b4 > temp_bytes) {
-        cudaFree(temp);
+        out.al.put(temp);
         temp = nullptr;
         temp_bytes = b4;
-        BCK(cudaMalloc(&temp, temp_bytes));
+        BCK(out.al.get(&temp, temp_bytes));
       }
       BCK(cudaMemsetAsync(flag + prev_nodes, 0, sizeof(uint32_t), s));
       b4 = temp_bytes;
@@ -283,12 +283,12 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
       P.n_dense = ndense;
       P.max_children = maxc;
       if (ndense > 0) {
-        BCK(cudaMalloc(&P.dense_slot, prev_nodes * sizeof(int32_t)));
+        BCK(out.al.get(&P.dense_slot, prev_nodes * sizeof(int32_t)));
         k_slots<<<grid_for(prev_nodes), 256, 0, s>>>(flag, excl, prev_nodes, P.dense_slot);
         BCK(cudaGetLastError());
-        BCK(cudaMalloc(&P.bitmap, (size_t)ndense * out.W * sizeof(uint32_t)));
+        BCK(out.al.get(&P.bitmap, (size_t)ndense * out.W * sizeof(uint32_t)));
         BCK(cudaMemsetAsync(P.bitmap, 0, (size_t)ndense * out.W * sizeof(uint32_t), s));
-        BCK(cudaMalloc(&P.rankdir, (size_t)ndense * out.R * sizeof(uint32_t)));
+        BCK(out.al.get(&P.rankdir, (size_t)ndense * out.R * sizeof(uint32_t)));
         k_fill_bitmap<<<grid_for(nodes), 256, 0, s>>>(C.label, parent, nodes, P.dense_slot, out.W,
                                                       P.bitmap);
         BCK(cudaGetLastError());
@@ -313,17 +313,17 @@ xgr_status trie_build(TrieHost& out, const int32_t* h_items, int64_t n, int V, i
   }
 
 fail:
-  cudaFree(d_items);
-  cudaFree(k0);
-  cudaFree(k1);
-  cudaFree(starts);
-  cudaFree(id_p);
-  cudaFree(id_d);
-  cudaFree(parent);
-  cudaFree(tmp);
-  cudaFree(d_err);
-  cudaFree(d_maxc);
-  cudaFree(temp);
+  out.al.put(d_items);
+  out.al.put(k0);
+  out.al.put(k1);
+  out.al.put(starts);
+  out.al.put(id_p);
+  out.al.put(id_d);
+  out.al.put(parent);
+  out.al.put(tmp);
+  out.al.put(d_err);
+  out.al.put(d_maxc);
+  out.al.put(temp);
   return st;
 }
 

@@ -351,7 +351,31 @@ struct LevelHost {
   int32_t max_children = 0;
 };
 
+// Device memory of a ctx: the caller's xgr_config.dev_alloc / dev_free hooks, else cudaMalloc /
+// cudaFree. Used only outside the step calls (init, mask build, host staging growth, destroy).
+struct DevAlloc {
+  void* (*alloc)(size_t, void*) = nullptr;
+  void (*release)(void*, void*) = nullptr;
+  void* user = nullptr;
+  template <typename T>
+  cudaError_t get(T** p, size_t bytes) const {
+    bytes = bytes < 16 ? 16 : bytes;
+    if (!alloc) return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    void* q = alloc(bytes, user);
+    *p = static_cast<T*>(q);
+    if (!q) return cudaErrorMemoryAllocation;
+    // every buffer is 16-byte aligned (TMA sources, vector loads); the hook must honour that
+    return (reinterpret_cast<uintptr_t>(q) & 15u) ? cudaErrorMisalignedAddress : cudaSuccess;
+  }
+  void put(void* p) const {
+    if (!p) return;
+    if (release) release(p, user);
+    else cudaFree(p);
+  }
+};
+
 struct TrieHost {
+  DevAlloc al;   // set by the ctx before the build; frees with the same hooks
   int V = 0, nd = 0, w = 0, W = 0, R = 0;
   int64_t n_items = 0;
   LevelHost lv[kMaxND + 1];

@@ -2073,11 +2073,6 @@ cudaError_t configure_stream_kernels() {
   if (const char* v = getenv("XGR_SEED_KERNEL")) g_seed_kernel = atoi(v);
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeSeedHist>, stream_smem<32, 2>())) != cudaSuccess) return e;
   if ((e = opt_in(k_stream<32, 1, 2, 3, kModeFused>, stream_smem<32, 2>())) != cudaSuccess) return e;
-  if ((e = opt_in(k_stream<16, 1, 4, 2, kModeNormal, __nv_bfloat16, 512>, stream_smem<16, 4, __nv_bfloat16, 512>())) !=
-      cudaSuccess)
-    return e;
-  if ((e = opt_in(k_stream<16, 1, 2, 2, kModeNormal, float, 512>, stream_smem<16, 2, float, 512>())) != cudaSuccess)
-    return e;
   if ((e = opt_in(k_stream<32, 1, 3, 2, kModeSeedReq>, stream_smem<32, 3>())) != cudaSuccess) return e;
 
   if ((e = opt_in(k_stream<32, 1, 4, 2, kModeSeedReq, __nv_bfloat16>, stream_smem<32, 4, __nv_bfloat16>())) !=
@@ -2168,10 +2163,7 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
       launch_pdl(k_seed_theta<256>, a.batch, 256, 0, s, a);
     }
     if (ev0) cudaEventRecord(ev0, s);
-    if (a.trie.V <= 8192 && g_stream_variant == 10)   // A/B: 512 threads x 16 tokens per row, 2 CTAs per SM
-      launch_pdl(k_stream<16, 1, 4, 2, kModeNormal, bf, 512>, std::min(total, 2 * sms), 512 + 32,
-                 stream_smem<16, 4, bf, 512>(), s, a, total, 0);
-    else if (a.trie.V <= 8192)
+    if (a.trie.V <= 8192)
       launch_pdl(k_stream<32, 1, 4, 3, kModeNormal, bf>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(), s,
           a, total, 0);
     else   // 16384-token rows: one 512-thread consumer group per SM, 4 x 32 KB stages
@@ -2230,10 +2222,6 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
         break;
       case 2:
         launch_pdl(k_stream<32, 1, 1, 4>, std::min(total, 4 * sms), 256 + 32, stream_smem<32, 1>(), s, a, total, seeded);
-        break;
-      case 11:   // A/B: 512 threads x 16 tokens per row, 2 CTAs per SM
-        launch_pdl(k_stream<16, 1, 2, 2, kModeNormal, float, 512>, std::min(total, 2 * sms), 512 + 32,
-                   stream_smem<16, 2, float, 512>(), s, a, total, seeded);
         break;
       default:  // three independent CTAs per SM, each a producer warp + one group, 2 stages
         launch_pdl(k_stream<32, 1, 2, 3>, std::min(total, 3 * sms), 256 + 32, stream_smem<32, 2>(), s, a, total, seeded);

@@ -107,3 +107,32 @@ def test_host_step_bf16_and_errors():
         binding.xgr_beam_step_host(bs.ctx, B, ctypes.c_void_p(x.data_ptr()), 7, BW, V, None)
     assert e.value.name == "XGR_ERR_UNSUPPORTED"
     bs.close()
+
+
+def test_host_logits_c2_full_size_bitwise():
+    """C2 at full size (dense steps over 8192 rows) through xgr_beam_step_host from pinned memory:
+    bitwise the device-logits path's states and outputs."""
+    import torch
+
+    import paper_2512_11529_b200 as xgr
+    from synth import config, make_items, make_logits_torch
+    c = config("C2")
+    items = make_items(c["n_items"], c["vocab"], c["nd"], c["trie_key"])
+    Bc, bw, Vc = c["batch"], c["beam_width"], c["vocab"]
+    steps = [make_logits_torch((Bc, 1 if t == 0 else bw, Vc), 11 * t + 1, 2.0) for t in range(c["nd"])]
+    res = []
+    for host in (False, True):
+        bs = xgr.BeamSearch(Vc, c["nd"], bw, Bc)
+        bs.mask_build(items)
+        per = []
+        for lg in steps:
+            bs.step(lg.cpu().pin_memory() if host else lg)
+            v = bs.view()
+            per.append({k: v[k].cpu().numpy().copy() for k in ("parent", "token", "score", "n_live")})
+        res.append((bs.finalize(on_device=False), per))
+        bs.close()
+    _same(res[0][0], res[1][0])
+    for a, b in zip(res[0][1], res[1][1]):
+        for k in a:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    torch.cuda.synchronize()

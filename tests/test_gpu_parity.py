@@ -377,6 +377,28 @@ def test_c2_full_size_all_requests(xgr):
     assert cnt["survivors"] <= 8 * 128 * 64, cnt
 
 
+def _with_seed_kernel(xgr, mode, fn):
+    """Runs fn() with XGR_SEED_KERNEL=mode (read by the library at every init; process-global), then
+    restores the default (1) by initialising a throwaway ctx."""
+    import os
+    os.environ["XGR_SEED_KERNEL"] = str(mode)
+    try:
+        return fn()
+    finally:
+        os.environ["XGR_SEED_KERNEL"] = "1"
+        xgr.BeamSearch(16, 2, 4, 1).close()
+        del os.environ["XGR_SEED_KERNEL"]
+
+
+@pytest.mark.parametrize("name", ["C2", pytest.param("C3", marks=pytest.mark.slow)])
+def test_fused_seed_full_size_all_requests(xgr, name):
+    """The seed fused into the streaming kernel (XGR_SEED_KERNEL=4, kModeFused: theta published by
+    the request's last seed row, waited for by its other rows): parity on every request."""
+    out, stats, bs = _with_seed_kernel(xgr, 4, lambda: _full(xgr, name))
+    assert np.all(out["n_live"] == config(name)["beam_width"])
+    assert bs.counters()["overflow"] == 0
+
+
 @pytest.mark.slow
 def test_c3_full_size_all_requests(xgr):
     out, stats, bs = _full(xgr, "C3")

@@ -17,7 +17,7 @@ steps = [make_logits_torch((B, 1 if t == 0 else BW, V), 90 + t, 2.0) for t in ra
 outs = []
 for mode in ("4", "1"):
     os.environ["XGR_SEED_KERNEL"] = mode
-    bs = xgr.BeamSearch(V, ND, BW, B, flags=2)
+    bs = xgr.BeamSearch(V, ND, BW, B, flags=2 | 4)   # counters, every step on the dense route
     bs.mask_build(items)
     for lg in steps:
         bs.step(lg)

@@ -79,3 +79,18 @@ def test_reference_arm_nonzero_rank_exits(monkeypatch):
     monkeypatch.setenv("RANK", "1")
     monkeypatch.setenv("WORLD_SIZE", "2")
     assert bench.main(["--impl", "reference"]) == 0
+
+
+def test_traffic_files_keyed_by_config_partition_dtype_sigma():
+    """Each bench line reads the ncu capture of its own config, partition, dtype and sigma, and
+    reports null when none is committed (never another config's file)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench.traffic_key("C3", "f32", 2.0) == "ncu_k_stream_C3_f32_traffic.json"
+    assert bench.traffic_key("C3", "bf16", 4.0) == "ncu_k_stream_C3_bf16_s4_traffic.json"
+    assert bench.traffic_key("C5", "f32", 2.0, "weak") == "ncu_k_stream_C5_weak_f32_traffic.json"
+    assert bench.committed_traffic("C9", "f32", 2.0) is None
+    for cfg, dt, sg, sp in (("C3", "f32", 2.0, ""), ("C5", "f32", 2.0, "weak")):
+        tr = bench.committed_traffic(cfg, dt, sg, sp)
+        assert tr is not None and tr["dram_bytes_per_launch"] > 0, (cfg, sp)
+        assert bench.traffic_key(cfg, dt, sg, sp) in tr["file"]

@@ -186,6 +186,15 @@ __device__ __forceinline__ float theta_value(uint32_t th) {
   return th == 0u ? -INFINITY : o2f(th);
 }
 
+// Shared-memory histogram increment, branch-free: `if (p) atomicAdd(&h[i], 1)` inside an unrolled
+// loop compiles to a divergent branch per element (BSSY/BSYNC/BRA; ptxas will not predicate a
+// shared atomic). Here every lane adds p (0 or 1): a lane with p false adds 0 to bin `lane` (distinct
+// addresses across lanes, no same-address serialisation among them).
+__device__ __forceinline__ void hist_inc_if(bool p, uint32_t* h, uint32_t i) {
+  const uint32_t addr = (uint32_t)__cvta_generic_to_shared(h + (p ? i : (threadIdx.x & 31u)));
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"((uint32_t)p) : "memory");
+}
+
 // Logit element loads: fp32 as is; bf16 widened exactly to fp32 (R19 / NEXT f1).
 __device__ __forceinline__ float ldx(const float* p) { return *p; }
 __device__ __forceinline__ float ldx(const __nv_bfloat16* p) {

@@ -224,6 +224,13 @@ __device__ __forceinline__ void warp_find_digit_desc(const uint32_t* hist, uint3
   }
 }
 
+// One compare-exchange of a sorting network, from the side of the element holding v with partner
+// o: keep the larger if keep_max, else the smaller. One 64-bit compare: (o > v) == keep_max selects
+// o; on equal keys (only the zero padding) both choices are the same value.
+__device__ __forceinline__ uint64_t ce_pick(uint64_t v, uint64_t o, bool keep_max) {
+  return ((o > v) == keep_max) ? o : v;
+}
+
 __device__ __forceinline__ uint64_t warp_sort_desc_u64(uint64_t v) {
   const int lane = lane_id();
 #pragma unroll
@@ -232,7 +239,7 @@ __device__ __forceinline__ uint64_t warp_sort_desc_u64(uint64_t v) {
     for (int stride = size >> 1; stride > 0; stride >>= 1) {
       const uint64_t o = __shfl_xor_sync(0xffffffffu, v, stride);
       const bool keep_max = ((lane & stride) == 0) == ((lane & size) == 0);
-      v = keep_max ? (o > v ? o : v) : (o < v ? o : v);
+      v = ce_pick(v, o, keep_max);
     }
   }
   return v;
@@ -373,10 +380,10 @@ __device__ void block_sort_desc(const uint64_t* src, int n, uint64_t* xbuf, uint
             if (s2 == stride && (j & s2) == 0) {
               const int jj = j | s2;
               const bool desc = ((EPT * tid + j) & size) == 0;
-              const uint64_t hi = v[j] > v[jj] ? v[j] : v[jj];
-              const uint64_t lo = v[j] > v[jj] ? v[jj] : v[j];
-              v[j] = desc ? hi : lo;
-              v[jj] = desc ? lo : hi;
+              const bool keep = (v[j] > v[jj]) == desc;   // v[j] already on its side
+              const uint64_t a0 = v[j], a1 = v[jj];
+              v[j] = keep ? a0 : a1;
+              v[jj] = keep ? a1 : a0;
             }
           }
         }
@@ -386,7 +393,7 @@ __device__ void block_sort_desc(const uint64_t* src, int n, uint64_t* xbuf, uint
           const int i = EPT * tid + j;
           const uint64_t o = __shfl_xor_sync(0xffffffffu, v[j], stride / EPT);
           const bool keep_max = ((i & stride) == 0) == ((i & size) == 0);
-          v[j] = keep_max ? (o > v[j] ? o : v[j]) : (o < v[j] ? o : v[j]);
+          v[j] = ce_pick(v[j], o, keep_max);
         }
       } else {
 #pragma unroll
@@ -397,7 +404,7 @@ __device__ void block_sort_desc(const uint64_t* src, int n, uint64_t* xbuf, uint
           const int i = EPT * tid + j;
           const uint64_t o = xbuf[i ^ stride];
           const bool keep_max = ((i & stride) == 0) == ((i & size) == 0);
-          v[j] = keep_max ? (o > v[j] ? o : v[j]) : (o < v[j] ? o : v[j]);
+          v[j] = ce_pick(v[j], o, keep_max);
         }
         __syncthreads();
       }
@@ -1239,7 +1246,7 @@ __global__ void __launch_bounds__(T, 2) k_sparse(const __grid_constant__ StepArg
           __syncthreads();
 #pragma unroll
           for (int k = 0; k < RPT; ++k)
-            if (kk[k]) atomicAdd(&hist[(uint32_t)(kk[k] >> 51)], 1u);
+            hist_inc_if(kk[k] != 0ull, hist, (uint32_t)(kk[k] >> 51));
           __syncthreads();
           // thread t owns bins 8191 - 16 t - j (j < 16): descending order over the block
           uint32_t c16[16], loc = 0;

@@ -698,10 +698,10 @@ __device__ __forceinline__ void seed_hist_row(const StepArgs& a) {
   if (cmax >= tau && cmax > -INFINITY) {
 #pragma unroll
     for (int e = 0; e < 4 * VPT; ++e) {
-      if (x[e] >= tau && x[e] > -INFINITY) {
-        const float dd = __fmul_rn(__fsub_rn(S0, x[e]), 128.0f);
-        if (dd >= 0.0f && dd < (float)kSeedBins) atomicAdd(&s_hist[(int)dd], 1u);
-      }
+      // -inf (illegal) gives dd = +inf, out of range; tau > -inf here
+      const float dd = __fmul_rn(__fsub_rn(S0, x[e]), 128.0f);
+      const bool in = x[e] >= tau && dd >= 0.0f && dd < (float)kSeedBins;
+      hist_inc_if(in, s_hist, in ? (uint32_t)(int)dd : 0u);
     }
   }
   __syncthreads();
@@ -2156,7 +2156,8 @@ cudaError_t launch_stream(const StepArgs& a, int rows, cudaStream_t s, cudaEvent
         if (a.trie.V <= 8192 && g_seed_kernel != 1 && !a.topk)
           launch_pdl(k_stream<32, 1, 4, 3, kModeSeedHist, bf>, std::min(ns, 3 * sms), 256 + 32, stream_smem<32, 4, bf>(),
                      s, a, ns, 0);
-        else if (a.trie.V <= 8192) launch_pdl(k_seed_hist<256, 4, bf>, dim3(a.batch, r0), 256, 0, s, a);
+        else if (a.trie.V <= 8192)
+          launch_pdl(k_seed_hist<256, 4, bf>, dim3(a.batch, r0), 256, 0, s, a);
         else launch_pdl(k_seed_hist<256, 8, bf>, dim3(a.batch, r0), 256, 0, s, a);
         ++*launches;
       }
